@@ -1,0 +1,427 @@
+#!/usr/bin/env python
+"""Benchmark of the auto-tuning hot path on B200 (bench contract).
+
+metric (BASELINE.json): "best-config GB/s or GFLOP/s per kernel vs B200
+roofline; configs benchmarked/sec".
+
+Workload (default, BASELINE.json configs[1]): hotspot 4096x4096 fp32,
+20 iterations, a stratified sweep over temporal_tiling_factor 1..10 of
+the paper's hotspot space.  One *step* = one batch of B configurations
+per rank, each run through the full protocol of the reference
+(`pkg/src/tunescape/measure.py:59-79`: 1 warmup + 7 timed runs, mean)
+with an L2 flush before every run (3x L2 buffer, outside the events),
+plus on-device verification against the naive reference kernel.
+
+* ``value``  -- configurations benchmarked per second over all ranks,
+  cubins already compiled (NVRTC ran in an untimed precompile phase; the
+  cold figure including compilation is reported as ``cold``).
+* ``e2e``    -- the same metric through the public API with HOST buffers:
+  every step re-uploads the inputs from pinned host memory and reads the
+  best configuration's output grid back.
+* ``roofline`` -- the best configuration's dominant launch against its
+  binding ceiling (HBM or FP32), measured with CUDA events in the run.
+* ``cpu_baseline`` -- the oracle port of the reference loop (CPU kernel,
+  all host threads) on a bounded sample, rank 0 only.
+
+``--impl reference`` times that CPU path alone and prints its own line.
+Under torchrun each rank takes a disjoint shard of configurations
+(weak scaling; no data-path collective), time = max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "hotspot": dict(param="temporal_tiling_factor", batch=40,
+                    desc="hotspot 4096x4096 fp32, 20 iterations, temporal_tiling_factor 1-10 sweep"),
+    "convolution": dict(param="tile_size_y", batch=24,
+                        desc="convolution 4096x4096 fp32, 15x15 filter"),
+    "dedispersion": dict(param="tile_size_y", batch=8,
+                         desc="dedispersion 1536 ch x 2048 DM x 25000 samples fp32"),
+    "gemm": dict(param="VWM", batch=12, desc="gemm 4096^3 fp32 CLBlast space"),
+}
+
+
+# ----------------------------------------------------------------------------
+# distributed plumbing (torch.distributed only for barrier / max / gather)
+
+
+class Dist:
+    def __init__(self):
+        self.world = int(os.environ.get("WORLD_SIZE", "1"))
+        self.rank = int(os.environ.get("RANK", "0"))
+        self.local = int(os.environ.get("LOCAL_RANK", "0"))
+        self.pg = None
+        if self.world > 1:
+            import torch
+            import torch.distributed as dist
+
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist, self.torch, self.backend = dist, torch, backend
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self._tensor([v])
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t[0])
+
+    def sum(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        t = self._tensor([v])
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM)
+        return float(t[0])
+
+    def gather_obj(self, obj):
+        if self.world == 1:
+            return [obj]
+        out = [None] * self.world
+        self.dist.all_gather_object(out, obj)
+        return out
+
+    def _tensor(self, vals):
+        dev = f"cuda:{self.local}" if self.backend == "nccl" else "cpu"
+        return self.torch.tensor(vals, dtype=self.torch.float64, device=dev)
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------------------
+# clocks sampled DURING the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------
+
+
+def parse_args(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="hotspot")
+    ap.add_argument("--batch", type=int, default=None, help="configurations per step per rank")
+    ap.add_argument("--seed", type=int, default=2407)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args(argv)
+
+
+def metric_name():
+    return "best-config GB/s or GFLOP/s per kernel vs B200 roofline; configs benchmarked/sec"
+
+
+def step_configs(space, wl, batch, seed, step, rank, world):
+    """Disjoint configurations for (step, rank): offset blocks of one permutation."""
+    from paper_2407_11488_b200.sweep import stratified_sample
+
+    offset = (step * world + rank) * batch
+    return stratified_sample(space, batch, seed, wl["param"], offset=offset)
+
+
+def run_cpu_baseline(workload: str, configs: list, budget_s: float, protocol_runs=(1, 7)) -> dict:
+    """Oracle port of the reference loop on the host (bounded sample)."""
+    from oracle import reference_port
+
+    return reference_port.timed_sample(workload, configs, budget_s=budget_s,
+                                       warmup=protocol_runs[0], runs=protocol_runs[1])
+
+
+def reference_arm(args, dist: Dist):
+    if dist.rank != 0:
+        return
+    from paper_2407_11488_b200.problems import make_problem
+
+    wl = WORKLOADS[args.workload]
+    prob = make_problem(args.workload)
+    per_step = []
+    total_cfg = 0
+    info = None
+    steps = args.warmup + args.steps
+    for s in range(steps):
+        cfgs = step_configs(prob.space, wl, 2, args.seed + 17, s, 0, 1)
+        r = run_cpu_baseline(args.workload, cfgs, budget_s=max(2.0, args.cpu_sample_s / steps))
+        info = r
+        if s >= args.warmup:
+            per_step.append(r["seconds"])
+            total_cfg += r["configs"]
+    secs = sum(per_step)
+    value = total_cfg / secs if secs > 0 else 0.0
+    line = {
+        "impl": "reference", "metric": metric_name(), "value": round(value, 4), "unit": "configs/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1000 * secs / max(1, args.steps), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": wl["desc"], "configs_per_step": 2, "protocol": "1 warmup + 7 runs, mean",
+                   "executor": "oracle port of the reference loop (C kernel, all host threads)"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "configs/s", "cores": info["cores"],
+                         "kind": "port", "sample": info["sample"]},
+        "e2e": {"value": round(value, 4), "unit": "configs/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def our_arm(args, dist: Dist):
+    from paper_2407_11488_b200 import runtime as rt
+    from paper_2407_11488_b200.cuda_backend import Compiler, CudaTarget
+    from paper_2407_11488_b200.measure import MeasurementProtocol
+    from paper_2407_11488_b200.problems import make_problem
+    from paper_2407_11488_b200.sweep import fp32_peak, measured_peaks, roofline
+    from paper_2407_11488_b200.paramspace import config_key
+
+    wl = WORKLOADS[args.workload]
+    batch = args.batch or wl["batch"]
+    cache_dir = tempfile.mkdtemp(prefix="tsg_cubins_")  # cold cache every run: honest cold numbers
+    compiler = Compiler(cache=rt.CubinCache(cache_dir))
+    dev = rt.Device(dist.local)
+    prob = make_problem(args.workload)
+    t_setup = time.perf_counter()
+    target = CudaTarget(prob, device=dev, compiler=compiler)
+    setup_s = time.perf_counter() - t_setup
+    proto = MeasurementProtocol(warmup_runs=1, benchmark_runs=7, flush_l2=True)
+    peaks = measured_peaks()
+    peaks.update(fp32_peak(dev))
+    space = prob.space
+
+    def run_step(configs):
+        obs = []
+        for i, c in enumerate(configs):
+            if i % 4 == 0:
+                target.prefetch(configs[i:])
+            obs.append((c, target.execute(c, proto)))
+        return obs
+
+    # -- warmup steps double as the COLD measurement (NVRTC pipelined) -------
+    cold_cfg, cold_s = 0, 0.0
+    for s in range(args.warmup):
+        cfgs = step_configs(space, wl, batch, args.seed, s, dist.rank, dist.world)
+        t0 = time.perf_counter()
+        run_step(cfgs)
+        cold_s += time.perf_counter() - t0
+        cold_cfg += len(cfgs)
+    dist.barrier()
+    cold_rate = dist.sum(cold_cfg) / dist.max(cold_s) if cold_s else 0.0
+
+    # -- precompile the timed steps' configurations (untimed) ----------------
+    timed_sets = [step_configs(space, wl, batch, args.seed, args.warmup + s, dist.rank, dist.world)
+                  for s in range(args.steps)]
+    t0 = time.perf_counter()
+    futs = [compiler.submit(target.source, prob.options(dict(zip(space.param_names, c))))
+            for cs in timed_sets for c in cs]
+    for f in futs:
+        f.result()
+    precompile_s = time.perf_counter() - t0
+
+    # -- timed region -----------------------------------------------------------
+    launches0 = dev.launch_count
+    sampler = ClockSampler(dist.local)
+    results = []
+    dist.barrier()
+    dev.mark(0)
+    sampler.start()
+    t_wall = time.perf_counter()
+    for cs in timed_sets:
+        results.extend(run_step(cs))
+    dev.mark(1)
+    elapsed_ms = dev.elapsed_ms(0, 1)
+    wall_s = time.perf_counter() - t_wall
+    clocks = sampler.stop()
+    dist.barrier()
+    launches = dev.launch_count - launches0
+    n_cfg = sum(len(cs) for cs in timed_sets)
+    t_max = dist.max(elapsed_ms)
+    total = dist.sum(n_cfg)
+    value = total / (t_max / 1000.0)
+
+    ok = [(c, o) for c, o in results if o.ok]
+    fails = {}
+    for _, o in results:
+        if not o.ok:
+            fails[o.status.value] = fails.get(o.status.value, 0) + 1
+    best_c, best_o = min(ok, key=lambda co: co[1].time_ms) if ok else (None, None)
+    best = None
+    roof = {}
+    if best_c is not None:
+        cfg = dict(zip(space.param_names, best_c))
+        info = target.extras.get(config_key(best_c), {})
+        roof = roofline(prob, cfg, info, peaks)
+        t = best_o.time_ms * 1e-3
+        best = {"config": cfg, "time_ms": round(best_o.time_ms, 5),
+                "gflops": round(prob.flops(cfg) / t / 1e9, 2),
+                "gbs_compulsory": round(prob.compulsory_bytes(cfg) / t / 1e9, 2),
+                "verify_rel_err": info.get("verify_rel_err")}
+    times = [o.time_ms for _, o in ok]
+    impact = None
+    if times:
+        perfs = [1.0 / t for t in times]
+        impact = {"best_over_median": round(max(perfs) / statistics.median(perfs), 3),
+                  "best_over_worst": round(max(perfs) / min(perfs), 3), "n_ok": len(times),
+                  "failed": fails}
+
+    # -- e2e: public API with host buffers -----------------------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = {b.name: b.init for b in prob.buffers() if b.init is not None}
+        pinned = {}
+        for k, arr in host.items():
+            pinned[k] = arr
+            dev.lib.tsg_host_register(arr.ctypes.data, arr.nbytes)
+        out_host = np.empty(prob.output_count, np.float32)
+        dev.lib.tsg_host_register(out_host.ctypes.data, out_host.nbytes)
+        h2d = sum(a.nbytes for a in pinned.values())
+        dist.barrier()
+        dev.mark(2)
+        e2e_cfg = 0
+        for cs in timed_sets:
+            for k, arr in pinned.items():
+                target.bufs[k].upload(arr)
+            obs = run_step(cs)
+            e2e_cfg += len(cs)
+            okb = [(c, o) for c, o in obs if o.ok]
+            if okb:
+                bc = min(okb, key=lambda co: co[1].time_ms)[0]
+                st, out = target.run_output(bc)
+                if st.value == "ok":
+                    out_host[:] = out
+        dev.mark(3)
+        e2e_ms = dist.max(dev.elapsed_ms(2, 3))
+        e2e = {"value": round(dist.sum(e2e_cfg) / (e2e_ms / 1000.0), 3), "unit": "configs/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_host.nbytes),
+               "path": "CudaTarget.execute per config (C-ABI tsg_run_timed) + inputs H2D from pinned "
+                       "host memory + best output D2H, every step"}
+        for arr in list(pinned.values()) + [out_host]:
+            dev.lib.tsg_host_unregister(arr.ctypes.data)
+
+    # -- CPU baseline (rank 0, N=1 only) -------------------------------------------------
+    cpu = None
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_cpu_baseline(args.workload, timed_sets[0][:4], budget_s=args.cpu_sample_s)
+            cpu = {"value": round(r["configs"] / r["seconds"], 4), "unit": "configs/s",
+                   "cores": r["cores"], "kind": "port", "sample": r["sample"]}
+        except Exception as e:  # noqa: BLE001 -- baseline is reported, never fatal
+            cpu = {"value": None, "unit": "configs/s", "cores": None, "kind": "port",
+                   "sample": f"unavailable: {e}"}
+
+    all_best = dist.gather_obj(best)
+    if dist.rank == 0:
+        line = {
+            "metric": metric_name(), "value": round(value, 3), "unit": "configs/s",
+            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(t_max / args.steps, 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wl["desc"], "configs_per_step_per_rank": batch,
+                       "protocol": "1 warmup + 7 timed runs per config, mean (tunescape default)",
+                       "l2": "flushed before every run (3x L2 buffer written, outside the events)",
+                       "compile": "NVRTC sm_100a; timed steps use cubins compiled in an untimed "
+                                  "precompile phase; cold (pipelined NVRTC) rate in 'cold'",
+                       "verify": "every config checked on-device vs the naive reference kernel",
+                       "parallelism": f"config shards x{dist.world} (no data-path collective)"},
+            "cold": {"value": round(cold_rate, 3), "unit": "configs/s",
+                     "compile_workers": compiler.pool._max_workers,
+                     "precompile_s": round(precompile_s, 3)},
+            "best_config": best, "best_config_per_rank": all_best if dist.world > 1 else None,
+            "tuning_impact": impact, "roofline": roof,
+            "peaks": {"hbm_gbs": peaks["hbm_gbs"], "hbm_source": peaks["source"],
+                      "fp32_tflops": round(peaks["fp32_tflops"], 3),
+                      "fp32_source": "measured in-run (kernels/peak.cu FFMA probe)"},
+            "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clocks,
+            "setup_s": round(setup_s, 2), "wall_s_timed": round(wall_s, 3),
+        }
+        print(json.dumps(line), flush=True)
+    target.close()
+    compiler.shutdown()
+
+
+def main(argv=None):
+    args = parse_args(argv)
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            reference_arm(args, dist)
+        else:
+            our_arm(args, dist)
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,171 @@
+/*
+ * tsgpu.h -- C ABI of libtsgpu.so, the B200 device layer of the tuner.
+ *
+ * The reference (tunescape, pure Python) has NO device layer: its only
+ * executors are the replay backend and the subprocess backend
+ * (pkg/src/tunescape/measure.py:170-186, :218-305) dispatched from
+ * measure() (:308-324).  This library is the in-process executor that
+ * slots in at that seam: one call compiles a configuration (what the
+ * command backend's external program did with its compiler), one loads
+ * it, one runs warmup+benchmark launches with per-run CUDA-event timing
+ * (the program's TUNE_TIME_MS lines, measure.py:189-203), and one
+ * verifies the output on the device.  Failures are returned as codes
+ * that map 1:1 onto the reference's Status enum (measure.py:38-43):
+ *
+ *   TSG_OK                 -> Status.OK
+ *   TSG_ERR_COMPILE        -> Status.COMPILE_FAILED   (NVRTC error)
+ *   TSG_ERR_INVALID        -> Status.INVALID          (launch rejected:
+ *                             too many threads/registers/smem)
+ *   TSG_ERR_RUNTIME        -> Status.RUNTIME_FAILED   (fault during run;
+ *                             the context is poisoned, respawn worker)
+ *   TSG_ERR_TIMEOUT        -> Status.TIMEOUT          (watchdog)
+ *   TSG_ERR_SETUP / TSG_ERR_ARG -> raised as DeviceError/ProtocolError
+ *                             in Python (never a Status).
+ *
+ * Ownership: the library owns device memory, modules and contexts
+ * behind opaque handles; the caller owns host buffers.  Only opaque
+ * handles and raw device addresses (uint64) cross the boundary.  All
+ * functions return an int status; tsg_last_error() gives the message
+ * of the last failure on the calling thread.
+ *
+ * Threading: tsg_compile is context-free and thread-safe (run it from a
+ * host compile pool); everything else takes a context and must not be
+ * called concurrently on the same context ("measurement on a single
+ * backend is strictly sequential").
+ */
+#ifndef TSGPU_H
+#define TSGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TSG_OK = 0,
+  TSG_ERR_COMPILE = 1,
+  TSG_ERR_INVALID = 2,
+  TSG_ERR_RUNTIME = 3,
+  TSG_ERR_TIMEOUT = 4,
+  TSG_ERR_SETUP = 5,
+  TSG_ERR_ARG = 6
+};
+
+typedef struct tsg_ctx tsg_ctx;
+typedef struct tsg_module tsg_module;
+typedef struct tsg_kernel tsg_kernel;
+
+/* One kernel launch of a (possibly multi-launch) timed run.  `args` is
+ * the cuLaunchKernel kernelParams array: one pointer per kernel
+ * parameter, pointing at the parameter's value.  cluster[] = {0,0,0} or
+ * {1,1,1} means no cluster launch. */
+typedef struct {
+  tsg_kernel* fn;
+  unsigned grid[3];
+  unsigned block[3];
+  unsigned cluster[3];
+  unsigned smem_bytes;
+  void** args;
+} tsg_launch_t;
+
+/* Device properties reported by tsg_device_info. */
+typedef struct {
+  char name[256];
+  int cc_major, cc_minor;
+  int sm_count;
+  int max_threads_per_block;
+  int max_smem_per_block_optin;
+  int max_smem_per_sm;
+  int l2_bytes;
+  int regs_per_sm;
+  int clock_khz;
+  int mem_clock_khz;
+  int mem_bus_bits;
+  size_t total_mem;
+} tsg_device_info_t;
+
+/* Version / diagnostics ------------------------------------------------ */
+const char* tsg_last_error(void);
+const char* tsg_error_string(int code);
+int tsg_nvrtc_version(int* major, int* minor);
+int tsg_driver_version(int* version);
+
+/* Context (replaces: nothing -- the reference has no device; ref seam is
+ * BackendDescriptor, measure.py:114-144) ---------------------------------- */
+int tsg_init(int device, tsg_ctx** ctx);
+int tsg_destroy(tsg_ctx* ctx);
+int tsg_device_info(tsg_ctx* ctx, tsg_device_info_t* info);
+/* Kernels launched through this context since tsg_init (evidence that
+ * the native path ran). */
+uint64_t tsg_launch_count(tsg_ctx* ctx);
+
+/* Compilation: CUDA C++ source -> sm_100a cubin via NVRTC.  Context
+ * free, thread safe.  `name_expr` may be NULL (extern "C" kernels) or a
+ * template instantiation expression whose lowered (mangled) name is
+ * written to `lowered` (size lowered_len).  The cubin is malloc'd and
+ * must be released with tsg_free_host.  Replaces the compile step that
+ * the reference delegates to the benchmark program behind
+ * `command_template` (measure.py:233-245). */
+int tsg_compile(const char* source, const char* program_name, const char* name_expr,
+                const char* const* options, int n_options, void** image,
+                size_t* image_bytes, char* lowered, size_t lowered_len, char* log,
+                size_t log_len);
+void tsg_free_host(void* p);
+
+/* Modules ---------------------------------------------------------------- */
+int tsg_module_load(tsg_ctx* ctx, const void* image, size_t image_bytes, tsg_module** mod);
+int tsg_module_unload(tsg_module* mod);
+int tsg_get_function(tsg_module* mod, const char* name, tsg_kernel** fn);
+/* Kernel Tuner `cmem_args`: copy host bytes into a __constant__ symbol. */
+int tsg_set_constant(tsg_module* mod, const char* symbol, const void* host, size_t bytes);
+int tsg_func_attrs(tsg_kernel* fn, int* num_regs, int* static_smem, int* max_threads,
+                   int* local_bytes);
+/* Opt in to >48 KiB dynamic shared memory (hotspot needs up to 64 KiB,
+ * ts/spaces/hotspot.spec:25). */
+int tsg_set_max_dynamic_smem(tsg_kernel* fn, int bytes);
+
+/* Device memory ------------------------------------------------------------ */
+int tsg_alloc(tsg_ctx* ctx, size_t bytes, uint64_t* dptr);
+int tsg_free(tsg_ctx* ctx, uint64_t dptr);
+int tsg_h2d(tsg_ctx* ctx, uint64_t dst, const void* src, size_t bytes);
+int tsg_d2h(tsg_ctx* ctx, void* dst, uint64_t src, size_t bytes);
+int tsg_d2d(tsg_ctx* ctx, uint64_t dst, uint64_t src, size_t bytes);
+int tsg_memset32(tsg_ctx* ctx, uint64_t dst, uint32_t value, size_t count);
+int tsg_host_register(void* p, size_t bytes);
+int tsg_host_unregister(void* p);
+
+/* Execution ---------------------------------------------------------------- */
+/* Run the launch sequence once, untimed, and synchronise (run_kernel). */
+int tsg_run(tsg_ctx* ctx, const tsg_launch_t* seq, int n_launch, double timeout_ms);
+/* The measurement protocol (measure.py:59-79): `warmup` unrecorded runs,
+ * then `runs` recorded runs, each run = the whole launch sequence
+ * bracketed by CUDA events on the context's stream.  With flush_l2 != 0
+ * a >L2-sized buffer is overwritten before every run, outside the
+ * events.  times_ms[runs] receives per-run device times. */
+int tsg_run_timed(tsg_ctx* ctx, const tsg_launch_t* seq, int n_launch, int warmup, int runs,
+                  int flush_l2, double timeout_ms, float* times_ms);
+/* Per-launch device times of the LAST timed run (n_launch floats), for
+ * roofline accounting of the dominant kernel. */
+int tsg_last_launch_times(tsg_ctx* ctx, float* times_ms, int n_launch);
+
+/* Stream markers for timing a whole region (e.g. one benchmark step of
+ * many configurations) on the context's stream: record event `slot`
+ * (0..15), then read the device time between two recorded slots (waits
+ * for the later one). */
+int tsg_event_record(tsg_ctx* ctx, int slot);
+int tsg_event_elapsed(tsg_ctx* ctx, int slot_begin, int slot_end, float* ms);
+
+/* On-device verification (Kernel Tuner `answer`/`atol`): compares
+ * float32 arrays `out` and `ref` of n elements.  Reports max |out-ref|,
+ * max |ref|, number of elements with |out-ref| > atol + rtol*|ref| and
+ * number of non-finite outputs. */
+int tsg_compare_f32(tsg_ctx* ctx, uint64_t out, uint64_t ref, size_t n, double rtol, double atol,
+                    double* max_abs_err, double* max_abs_ref, uint64_t* n_bad,
+                    uint64_t* n_nonfinite);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSGPU_H */

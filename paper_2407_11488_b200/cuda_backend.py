@@ -1,0 +1,279 @@
+"""In-process B200 executor behind the ``cuda`` backend kind.
+
+One :class:`CudaTarget` = one problem instance resident in HBM on one
+GPU.  ``execute(config, protocol)`` is the B200 replacement of the
+reference's ``command_execute`` (`pkg/src/tunescape/measure.py:218-305`):
+
+1. NVRTC -> sm_100a cubin (host compile pool + on-disk cubin cache),
+   failure -> ``compile_failed`` with the NVRTC log in ``detail``;
+2. ``cuModuleLoadData``, ``__constant__`` upload, dynamic-smem opt-in,
+   failure -> ``invalid``;
+3. warmup + benchmark runs in ONE native call, per-run CUDA events on
+   the launch stream, optional L2 flush outside the events; a rejected
+   launch -> ``invalid``, a device fault -> ``runtime_failed`` (the
+   context is poisoned; the multi-GPU runner respawns the worker), the
+   watchdog -> ``timeout``;
+4. on-device verification against the answer buffer (no D2H of the
+   output), mismatch -> ``runtime_failed`` with the error in ``detail``.
+
+Compilation is pipelined: :meth:`prefetch` queues configurations on a
+thread pool (ctypes releases the GIL, NVRTC is thread-safe) while the
+GPU times earlier ones.
+"""
+
+from __future__ import annotations
+
+import os
+import threading
+import time
+from collections import OrderedDict
+from concurrent.futures import Future, ThreadPoolExecutor
+
+import numpy as np
+
+from . import runtime as rt
+from .errors import DeviceError
+from .measure import MeasurementProtocol, Observation, Status, aggregate_times
+from .paramspace import config_key
+
+_RC_STATUS = {rt.ERR_COMPILE: Status.COMPILE_FAILED, rt.ERR_INVALID: Status.INVALID,
+              rt.ERR_RUNTIME: Status.RUNTIME_FAILED, rt.ERR_TIMEOUT: Status.TIMEOUT,
+              rt.ERR_ARG: Status.INVALID}
+
+
+def default_workers() -> int:
+    env = os.environ.get("TSG_COMPILE_WORKERS")
+    if env:
+        return max(1, int(env))
+    try:
+        n = len(os.sched_getaffinity(0))
+    except AttributeError:
+        n = os.cpu_count() or 1
+    return max(1, n - 1)
+
+
+class Compiler:
+    """Thread pool + cubin cache; futures resolve to CompileResult."""
+
+    def __init__(self, workers: int | None = None, cache: rt.CubinCache | None = None):
+        self.pool = ThreadPoolExecutor(max_workers=workers or default_workers(),
+                                       thread_name_prefix="nvrtc")
+        self.cache = cache if cache is not None else rt.CubinCache()
+        self._inflight: dict = {}
+        self._lock = threading.Lock()
+        self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "failed": 0}
+
+    def _job(self, source: str, options: list, key: str) -> rt.CompileResult:
+        hit = self.cache.get(key)
+        if hit is not None:
+            with self._lock:
+                self.stats["cache_hits"] += 1
+            return rt.CompileResult(True, hit[0], lowered=hit[1])
+        res = rt.compile_source(source, options)
+        with self._lock:
+            self.stats["compiled"] += 1
+            self.stats["compile_s"] += res.seconds
+            if not res.ok:
+                self.stats["failed"] += 1
+        if res.ok:
+            self.cache.put(key, res.image, res.lowered)
+        return res
+
+    def submit(self, source: str, options: list) -> Future:
+        key = self.cache.key(source, options, None)
+        with self._lock:
+            fut = self._inflight.get(key)
+            if fut is None:
+                fut = self.pool.submit(self._job, source, options, key)
+                self._inflight[key] = fut
+                fut.add_done_callback(lambda _f, k=key: self._drop(k))
+        return fut
+
+    def _drop(self, key):
+        with self._lock:
+            self._inflight.pop(key, None)
+
+    def compile(self, source: str, options: list) -> rt.CompileResult:
+        return self.submit(source, options).result()
+
+    def shutdown(self):
+        self.pool.shutdown(wait=False, cancel_futures=True)
+
+
+class CudaTarget:
+    """A problem instance resident on one GPU, measurable per config."""
+
+    def __init__(self, problem, device: rt.Device | int | None = None,
+                 compiler: Compiler | None = None, verify: bool = True,
+                 answer: np.ndarray | None = None, prefetch_depth: int | None = None):
+        self.problem = problem
+        if device is None or isinstance(device, int):
+            device = rt.Device(device or 0)
+        self.dev = device
+        self.compiler = compiler or Compiler()
+        self.verify = verify
+        self.source = problem.source()
+        self.bufs = {}
+        for spec in problem.buffers():
+            buf = self.dev.alloc(spec.nbytes)
+            if spec.init is not None:
+                buf.upload(spec.init)
+            self.bufs[spec.name] = buf
+        self.out = self.bufs[problem.output_name]
+        self.n_out = problem.output_count
+        self.answer_buf = None
+        if verify:
+            self.answer_buf = self.dev.alloc(self.n_out * 4)
+            if answer is not None:
+                self.answer_buf.upload(np.ascontiguousarray(answer, dtype=np.float32))
+            else:
+                self._compute_answer()
+        self.extras: dict = {}
+        self._pending: "OrderedDict[str, Future]" = OrderedDict()
+        self.prefetch_depth = prefetch_depth or 4 * self.compiler.pool._max_workers
+        self.stats = {"executed": 0, "gpu_ms": 0.0, "verify_failed": 0}
+
+    # -- answer ------------------------------------------------------------------
+    def _load(self, image: bytes):
+        rc, mod = self.dev.load(image)
+        if rc != rt.OK:
+            raise DeviceError(f"cannot load module: {mod}")
+        for sym, data in self.problem.constants().items():
+            rc = mod.set_constant(sym, data)
+            if rc != rt.OK:
+                raise DeviceError(f"cannot set constant {sym}: {rt.last_error()}")
+        return mod
+
+    def _compute_answer(self):
+        res = self.compiler.compile(self.source, self.problem.options(None) + ["-DREFERENCE_ONLY=1"])
+        if not res.ok:
+            raise DeviceError(f"reference kernel failed to compile:\n{res.error}")
+        mod = self._load(res.image)
+        try:
+            kern = mod.function(self.problem.reference_kernel)
+            bufs = dict(self.bufs)
+            bufs[self.problem.output_name] = self.answer_buf
+            launches = self.problem.reference_launches(kern, bufs)
+            rc, err = self.dev.run(launches, timeout_ms=600_000)
+            if rc != rt.OK:
+                raise DeviceError(f"reference kernel failed: {err}")
+        finally:
+            mod.unload()
+
+    def answer(self) -> np.ndarray:
+        out = np.empty(self.n_out, dtype=np.float32)
+        return self.answer_buf.download(out)
+
+    # -- compile pipeline ------------------------------------------------------------
+    def _options(self, cfg: dict) -> list:
+        return self.problem.options(cfg)
+
+    def prefetch(self, configs) -> None:
+        """Queue compilation of upcoming configurations (bounded window)."""
+        names = self.problem.space.param_names
+        for config in configs:
+            if len(self._pending) >= self.prefetch_depth:
+                break
+            key = config_key(config)
+            if key not in self._pending:
+                cfg = dict(zip(names, config))
+                self._pending[key] = self.compiler.submit(self.source, self._options(cfg))
+
+    def _compiled(self, key: str, cfg: dict) -> rt.CompileResult:
+        fut = self._pending.pop(key, None)
+        if fut is None:
+            fut = self.compiler.submit(self.source, self._options(cfg))
+        return fut.result()
+
+    # -- the protocol ------------------------------------------------------------------
+    def execute(self, config, protocol: MeasurementProtocol) -> Observation:
+        if self.dev.poisoned:
+            return Observation(Status.RUNTIME_FAILED,
+                               detail="device context poisoned by an earlier fault")
+        names = self.problem.space.param_names
+        cfg = dict(zip(names, config))
+        key = config_key(config)
+        info = {}
+        t0 = time.perf_counter()
+        res = self._compiled(key, cfg)
+        info["compile_wait_s"] = time.perf_counter() - t0
+        if not res.ok:
+            return Observation(Status.COMPILE_FAILED, detail=(res.error or res.log)[-2000:])
+        rc, mod = self.dev.load(res.image)
+        if rc != rt.OK:
+            return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(mod))
+        try:
+            for sym, data in self.problem.constants().items():
+                if mod.set_constant(sym, data) != rt.OK:
+                    return Observation(Status.RUNTIME_FAILED, detail=rt.last_error())
+            kern = mod.function(self.problem.kernel_name)
+            smem = self.problem.smem_bytes(cfg)
+            if smem > 48 * 1024:
+                if kern.set_max_dynamic_smem(smem) != rt.OK:
+                    return Observation(Status.INVALID, detail=rt.last_error())
+            info.update(kern.attrs())
+            info["smem_bytes"] = smem
+            launches = self.problem.launches(cfg, kern, self.bufs)
+            if self.verify:
+                # poison the output so a kernel that skips elements fails
+                self.dev._check(self.dev.lib.tsg_memset32(self.dev.ctx, self.out.ptr,
+                                                          0x7FC00000, self.n_out))
+            rc, times = self.dev.run_timed(launches, protocol.warmup_runs,
+                                           protocol.benchmark_runs, protocol.flush_l2,
+                                           protocol.timeout_ms)
+            if rc != rt.OK:
+                return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(times))
+            info["launch_ms"] = self.dev.last_launch_times(len(launches))
+            info["n_launches"] = len(launches)
+            if self.verify:
+                cmp = self.dev.compare(self.out, self.answer_buf, self.n_out,
+                                       self.problem.rtol, self.problem.atol)
+                info["verify"] = cmp
+                rel = cmp["max_abs_err"] / cmp["max_abs_ref"] if cmp["max_abs_ref"] > 0 else \
+                    cmp["max_abs_err"]
+                info["verify_rel_err"] = rel
+                if cmp["n_nonfinite"] or rel > self.problem.rtol:
+                    self.stats["verify_failed"] += 1
+                    return Observation(
+                        Status.RUNTIME_FAILED,
+                        detail=(f"verification failed: max_abs_err={cmp['max_abs_err']:.3e} "
+                                f"max_abs_ref={cmp['max_abs_ref']:.3e} "
+                                f"nonfinite={cmp['n_nonfinite']} bad={cmp['n_bad']}"),
+                    )
+        finally:
+            mod.unload()
+            self.extras[key] = info
+        self.stats["executed"] += 1
+        self.stats["gpu_ms"] += sum(times)
+        return Observation(Status.OK, times_ms=tuple(times),
+                           time_ms=aggregate_times(protocol, times))
+
+    def run_output(self, config) -> tuple:
+        """Run one configuration once and return (Observation-like status, host output)."""
+        names = self.problem.space.param_names
+        cfg = dict(zip(names, config))
+        res = self._compiled(config_key(config), cfg)
+        if not res.ok:
+            return Status.COMPILE_FAILED, res.error
+        mod = self._load(res.image)
+        try:
+            kern = mod.function(self.problem.kernel_name)
+            smem = self.problem.smem_bytes(cfg)
+            if smem > 48 * 1024 and kern.set_max_dynamic_smem(smem) != rt.OK:
+                return Status.INVALID, rt.last_error()
+            self.dev._check(self.dev.lib.tsg_memset32(self.dev.ctx, self.out.ptr, 0x7FC00000,
+                                                      self.n_out))
+            rc, err = self.dev.run(self.problem.launches(cfg, kern, self.bufs))
+            if rc != rt.OK:
+                return _RC_STATUS.get(rc, Status.RUNTIME_FAILED), err
+            out = np.empty(self.n_out, dtype=np.float32)
+            self.out.download(out)
+            return Status.OK, out
+        finally:
+            mod.unload()
+
+    def close(self):
+        for b in self.bufs.values():
+            b.free()
+        if self.answer_buf:
+            self.answer_buf.free()

@@ -1,0 +1,539 @@
+"""The paper's four tunable benchmark problems on B200.
+
+Each :class:`Problem` fixes, for one bundled space
+(`paper_2407_11488_b200/spaces/*.spec`, identical to ref
+`ts/spaces/*.spec`):
+
+* the synthetic inputs (seeded, fp32) and their HBM layout,
+* the NVRTC source and the ``-D`` macros a configuration maps to,
+* the launch sequence of ONE benchmark run (hotspot: ceil(20/T)
+  launches with ping-pong buffers; the others: one launch),
+* the naive reference kernel that produces the on-device answer,
+* the algorithmic work (FLOP, compulsory bytes) used for roofline
+  accounting, and the verification tolerance.
+
+The reference holds none of this: tunescape only has the spaces
+(`SURVEY.md` §0.5); kernel definitions follow the paper's BAT / CLBlast
+kernels (`PAPER.md:141`) as restated in SURVEY.md §8(a) row a19.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from pathlib import Path
+
+import numpy as np
+
+from .paramspace import SearchSpaceSpec, bundled_space
+
+KDIR = Path(__file__).resolve().parent / "kernels"
+
+
+def _src(name: str) -> str:
+    return (KDIR / name).read_text()
+
+
+@dataclass
+class BufferSpec:
+    name: str
+    nbytes: int
+    init: np.ndarray | None = None  # host data uploaded at setup (None = scratch)
+
+
+class Problem:
+    """Base class; subclasses define one benchmark kernel family."""
+
+    space_name: str = ""
+    source_file: str = ""
+    kernel_name: str = ""
+    reference_kernel: str = ""
+    rtol: float = 1e-5
+    atol: float = 0.0
+    extra_options: tuple = ()
+
+    def __init__(self):
+        self.space: SearchSpaceSpec = bundled_space(self.space_name)
+        self._host = None
+
+    # -- inputs --------------------------------------------------------------
+    def host_buffers(self) -> list:
+        raise NotImplementedError
+
+    def buffers(self) -> list:
+        if self._host is None:
+            self._host = self.host_buffers()
+        return self._host
+
+    def constants(self) -> dict:
+        """``__constant__`` symbol -> host array (Kernel Tuner cmem_args)."""
+        return {}
+
+    @property
+    def output_name(self) -> str:
+        return "out"
+
+    @property
+    def output_count(self) -> int:
+        raise NotImplementedError
+
+    # -- compilation -----------------------------------------------------------
+    def source(self) -> str:
+        return _src(self.source_file)
+
+    def problem_defines(self) -> dict:
+        return {}
+
+    def config_defines(self, cfg: dict) -> dict:
+        return {k.upper(): int(v) for k, v in cfg.items()}
+
+    def options(self, cfg: dict | None) -> list:
+        opts = ["--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"] + list(self.extra_options)
+        d = dict(self.problem_defines())
+        if cfg is not None:
+            d.update(self.config_defines(cfg))
+        opts += [f"-D{k}={v}" for k, v in sorted(d.items())]
+        return opts
+
+    # -- execution ---------------------------------------------------------------
+    def smem_bytes(self, cfg: dict) -> int:
+        return 0
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        raise NotImplementedError
+
+    def reference_launches(self, kernel, bufs: dict) -> list:
+        raise NotImplementedError
+
+    # -- work accounting -----------------------------------------------------------
+    def flops(self, cfg: dict | None = None) -> float:
+        return 0.0
+
+    def compulsory_bytes(self, cfg: dict | None = None) -> float:
+        return 0.0
+
+    def describe(self) -> dict:
+        return {}
+
+
+def _u64(buf) -> C.c_uint64:
+    return C.c_uint64(buf.ptr)
+
+
+# =============================================================================
+# Convolution
+
+
+class Convolution(Problem):
+    """out[y][x] = sum_{i,j<15} in[y+i][x+j] * f[i][j].
+
+    HBM layout: input fp32 [(H+FH-1)+8 rows][IN_PITCH], IN_PITCH =
+    round_up(W+FW-1, 4) so every row starts 16-byte aligned (float4 /
+    TMA-friendly); 8 zero rows of slack let register-tiled threads read
+    past the last row without guards.  Output fp32 [H][W] dense.
+    Inputs: U[0,1) image (seed 1), U[0,1) filter (seed 2).
+    """
+
+    space_name = "convolution"
+    source_file = "convolution.cu"
+    kernel_name = "convolution_kernel"
+    reference_kernel = "convolution_reference"
+    rtol = 1e-5
+
+    def __init__(self, width: int = 4096, height: int = 4096, fw: int = 15, fh: int = 15,
+                 seed_image: int = 1, seed_filter: int = 2):
+        super().__init__()
+        self.W, self.H, self.FW, self.FH = width, height, fw, fh
+        self.in_w, self.in_h = width + fw - 1, height + fh - 1
+        self.pitch = ((self.in_w + 3) // 4) * 4
+        self.rows = self.in_h + 8
+        self.seed_image, self.seed_filter = seed_image, seed_filter
+
+    def image(self) -> np.ndarray:
+        return np.random.default_rng(self.seed_image).random((self.in_h, self.in_w), dtype=np.float32)
+
+    def filter(self) -> np.ndarray:
+        return np.random.default_rng(self.seed_filter).random((self.FH, self.FW), dtype=np.float32)
+
+    def host_buffers(self) -> list:
+        padded = np.zeros((self.rows, self.pitch), dtype=np.float32)
+        padded[: self.in_h, : self.in_w] = self.image()
+        return [BufferSpec("in", padded.nbytes, padded), BufferSpec("out", self.W * self.H * 4)]
+
+    def constants(self) -> dict:
+        return {"d_filter": self.filter().ravel()}
+
+    @property
+    def output_count(self) -> int:
+        return self.W * self.H
+
+    def problem_defines(self) -> dict:
+        return dict(IMG_W=self.W, IMG_H=self.H, FW=self.FW, FH=self.FH, IN_PITCH=self.pitch)
+
+    def config_defines(self, cfg: dict) -> dict:
+        return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
+                    TSY=cfg["tile_size_y"], READ_ONLY=cfg["read_only"],
+                    USE_PADDING=cfg["use_padding"], USE_SHMEM=cfg["use_shmem"])
+
+    def smem_bytes(self, cfg: dict) -> int:
+        if not cfg["use_shmem"]:
+            return 0
+        tw = cfg["block_size_x"] * cfg["tile_size_x"]
+        th = cfg["block_size_y"] * cfg["tile_size_y"]
+        w4 = ((tw + self.FW - 1 + 3) // 4) * 4
+        pitch = w4 + (1 if cfg["use_padding"] else 0)
+        return (th + self.FH - 1) * pitch * 4
+
+    def grid(self, cfg: dict) -> tuple:
+        tw = cfg["block_size_x"] * cfg["tile_size_x"]
+        th = cfg["block_size_y"] * cfg["tile_size_y"]
+        return (math.ceil(self.W / tw), math.ceil(self.H / th), 1)
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        return [Launch(kernel, self.grid(cfg), (cfg["block_size_x"], cfg["block_size_y"], 1),
+                       [_u64(bufs["out"]), _u64(bufs["in"])], smem=self.smem_bytes(cfg))]
+
+    def reference_launches(self, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        return [Launch(kernel, (math.ceil(self.W / 32), math.ceil(self.H / 8), 1), (256, 1, 1),
+                       [_u64(bufs["out"]), _u64(bufs["in"])])]
+
+    def flops(self, cfg=None) -> float:
+        return 2.0 * self.W * self.H * self.FW * self.FH
+
+    def compulsory_bytes(self, cfg=None) -> float:
+        return 4.0 * (self.in_w * self.in_h + self.W * self.H + self.FW * self.FH)
+
+    def describe(self) -> dict:
+        return {"image": f"{self.W}x{self.H}", "filter": f"{self.FW}x{self.FH}", "dtype": "fp32"}
+
+
+# =============================================================================
+# Hotspot
+
+
+def rodinia_constants(rows: int, cols: int, cell_m: float = 0.016 / 512) -> dict:
+    """Rodinia hotspot physical constants -> the kernel's fp32 coefficients.
+
+    Rodinia derives the per-cell geometry from a 0.016 m chip split into
+    rows x cols cells; at 4096^2 that makes the explicit scheme unstable
+    (sdc*r ~ 2.2 > 1/4).  We keep Rodinia's formulas but pin the CELL size
+    to Rodinia's 512^2 default (0.016/512 m), i.e. a proportionally larger
+    chip, so the 20-step run stays physical.  Unpinned by the reference
+    (SURVEY 8a a19); DESIGN.md records the choice.
+    """
+    max_pd, precision, spec_heat_si, k_si, factor_chip = 3.0e6, 0.001, 1.75e6, 100.0, 0.5
+    t_chip, amb = 0.0005, 80.0
+    gh = gw = cell_m
+    cap = factor_chip * spec_heat_si * t_chip * gw * gh
+    rx = gw / (2.0 * k_si * t_chip * gh)
+    ry = gh / (2.0 * k_si * t_chip * gw)
+    rz = t_chip / (k_si * gh * gw)
+    max_slope = max_pd / (factor_chip * t_chip * spec_heat_si)
+    step = precision / max_slope
+    f32 = lambda v: float(np.float32(v))  # noqa: E731
+    return dict(sdc=f32(step / cap), rx1=f32(1.0 / rx), ry1=f32(1.0 / ry), rz1=f32(1.0 / rz),
+                amb=f32(amb))
+
+
+class Hotspot(Problem):
+    """Rodinia hotspot, ``iterations`` explicit steps on a GH x GW grid.
+
+    One benchmark run = ceil(iterations / T) launches (T =
+    temporal_tiling_factor), the last advancing the remainder; buffers
+    ping-pong between ``tmp`` and ``out`` so the pristine input ``temp``
+    is never overwritten (every run does identical work) and the final
+    state always lands in ``out``.
+    Inputs: temp = 323.15 + U[0,10) (seed 3), power =
+    U[0,1)*1e-3 (seed 4), fp32 [GH][GW].
+    """
+
+    space_name = "hotspot"
+    source_file = "hotspot.cu"
+    kernel_name = "hotspot_kernel"
+    reference_kernel = "hotspot_reference"
+    rtol = 1e-5
+    extra_options = ("--fmad=false",)
+    FLOP_PER_CELL = 14
+
+    def __init__(self, width: int = 4096, height: int = 4096, iterations: int = 20,
+                 seed_temp: int = 3, seed_power: int = 4):
+        super().__init__()
+        self.W, self.H, self.iterations = width, height, iterations
+        self.seed_temp, self.seed_power = seed_temp, seed_power
+        self.k = rodinia_constants(height, width)
+
+    def temperature(self) -> np.ndarray:
+        rng = np.random.default_rng(self.seed_temp)
+        return (np.float32(323.15) + rng.random((self.H, self.W), dtype=np.float32) * np.float32(10.0))
+
+    def power(self) -> np.ndarray:
+        rng = np.random.default_rng(self.seed_power)
+        return rng.random((self.H, self.W), dtype=np.float32) * np.float32(1e-3)
+
+    def host_buffers(self) -> list:
+        n = self.W * self.H * 4
+        return [BufferSpec("temp", n, self.temperature()), BufferSpec("power", n, self.power()),
+                BufferSpec("tmp", n), BufferSpec("out", n)]
+
+    @property
+    def output_count(self) -> int:
+        return self.W * self.H
+
+    def problem_defines(self) -> dict:
+        return dict(GW=self.W, GH=self.H)
+
+    def config_defines(self, cfg: dict) -> dict:
+        return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
+                    TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
+                    UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"])
+
+    def smem_bytes(self, cfg: dict) -> int:
+        t = cfg["temporal_tiling_factor"]
+        ew = cfg["block_size_x"] * cfg["tile_size_x"] + 2 * t
+        eh = cfg["block_size_y"] * cfg["tile_size_y"] + 2 * t
+        return (2 + cfg["sh_power"]) * ew * eh * 4
+
+    def step_plan(self, t: int) -> list:
+        n = math.ceil(self.iterations / t)
+        return [t] * (n - 1) + [self.iterations - t * (n - 1)]
+
+    def _coeff_args(self):
+        k = self.k
+        return [C.c_float(k["sdc"]), C.c_float(k["rx1"]), C.c_float(k["ry1"]),
+                C.c_float(k["rz1"]), C.c_float(k["amb"])]
+
+    def _chain(self, kernel, bufs, n_launch, make):
+        """Buffers for a ping-pong chain ending in bufs['out']."""
+        seq = []
+        src = bufs["temp"]
+        for i in range(n_launch):
+            dst = bufs["out"] if (n_launch - 1 - i) % 2 == 0 else bufs["tmp"]
+            seq.append(make(i, src, dst))
+            src = dst
+        return seq
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        plan = self.step_plan(cfg["temporal_tiling_factor"])
+        ow = cfg["block_size_x"] * cfg["tile_size_x"]
+        oh = cfg["block_size_y"] * cfg["tile_size_y"]
+        grid = (math.ceil(self.W / ow), math.ceil(self.H / oh), 1)
+        block = (cfg["block_size_x"], cfg["block_size_y"], 1)
+        smem = self.smem_bytes(cfg)
+        return self._chain(kernel, bufs, len(plan), lambda i, s, d: Launch(
+            kernel, grid, block, [_u64(d), _u64(s), _u64(bufs["power"]), C.c_int(plan[i])]
+            + self._coeff_args(), smem=smem))
+
+    def reference_launches(self, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        grid = (math.ceil(self.W / 32), math.ceil(self.H / 8), 1)
+        return self._chain(kernel, bufs, self.iterations, lambda i, s, d: Launch(
+            kernel, grid, (256, 1, 1), [_u64(d), _u64(s), _u64(bufs["power"])]
+            + self._coeff_args()))
+
+    def flops(self, cfg=None) -> float:
+        return float(self.FLOP_PER_CELL) * self.W * self.H * self.iterations
+
+    def compulsory_bytes(self, cfg=None) -> float:
+        t = cfg["temporal_tiling_factor"] if cfg else 1
+        return 12.0 * self.W * self.H * len(self.step_plan(t))
+
+    def describe(self) -> dict:
+        return {"grid": f"{self.W}x{self.H}", "iterations": self.iterations, "dtype": "fp32"}
+
+
+# =============================================================================
+# Dedispersion
+
+
+K_DM = 4148.808  # s MHz^2 pc^-1 cm^3
+
+
+def dm_delay_table(nch: int, f_min_mhz: float, ch_bw_mhz: float, t_samp_s: float) -> np.ndarray:
+    """Per-channel delay in samples per unit DM (fp32), channel 0 = lowest.
+
+    delay[ch] = K_DM * (f_ch^-2 - f_max^-2) / t_samp, f_ch = f_min + ch*bw.
+    Constants are unpinned by the reference; DESIGN.md fixes
+    an L-band LOFAR/Apertif-like setup.
+    """
+    f = f_min_mhz + ch_bw_mhz * np.arange(nch, dtype=np.float64)
+    fmax = f[-1]
+    return (K_DM * (f ** -2 - fmax ** -2) / t_samp_s).astype(np.float32)
+
+
+def dm_shifts(delay: np.ndarray, ndm: int, dm_first: float, dm_step: float) -> np.ndarray:
+    """int32 [ndm][nch] shifts with the kernel's exact fp32 rounding."""
+    d = np.arange(ndm, dtype=np.float32)
+    dmv = (np.float32(dm_first) + d * np.float32(dm_step)).astype(np.float32)
+    prod = (dmv[:, None] * delay[None, :]).astype(np.float32)
+    return np.trunc(prod).astype(np.int32)
+
+
+class Dedispersion(Problem):
+    """out[dm][s] = sum_ch in[ch][s + shift(dm, ch)].
+
+    HBM layout: input fp32 [NCH][IN_PITCH] with IN_PITCH = round_up(NSAMP
+    + max_shift + 128, 32) (zero tail: grid overshoot reads stay in the
+    row), output fp32 [NDM][NSAMP].  Inputs U[0,1) (seed 5).
+    """
+
+    space_name = "dedispersion"
+    source_file = "dedispersion.cu"
+    kernel_name = "dedispersion_kernel"
+    reference_kernel = "dedispersion_reference"
+    rtol = 1e-5
+
+    def __init__(self, channels: int = 1536, samples: int = 25000, dms: int = 2048,
+                 f_min_mhz: float = 1425.0, ch_bw_mhz: float = 0.1953125,
+                 t_samp_s: float = 40.96e-6, dm_first: float = 0.0, dm_step: float = 0.02,
+                 seed: int = 5):
+        super().__init__()
+        self.NCH, self.NSAMP, self.NDM = channels, samples, dms
+        self.dm_first, self.dm_step = float(np.float32(dm_first)), float(np.float32(dm_step))
+        self.delay = dm_delay_table(channels, f_min_mhz, ch_bw_mhz, t_samp_s)
+        self.max_shift = int(dm_shifts(self.delay, dms, self.dm_first, self.dm_step).max())
+        self.in_w = samples + self.max_shift
+        self.pitch = ((samples + self.max_shift + 128 + 31) // 32) * 32
+        self.seed = seed
+
+    def data(self) -> np.ndarray:
+        return np.random.default_rng(self.seed).random((self.NCH, self.in_w), dtype=np.float32)
+
+    def host_buffers(self) -> list:
+        padded = np.zeros((self.NCH, self.pitch), dtype=np.float32)
+        padded[:, : self.in_w] = self.data()
+        return [BufferSpec("in", padded.nbytes, padded), BufferSpec("out", self.NDM * self.NSAMP * 4)]
+
+    def constants(self) -> dict:
+        return {"d_delay": self.delay}
+
+    @property
+    def output_count(self) -> int:
+        return self.NDM * self.NSAMP
+
+    def problem_defines(self) -> dict:
+        return dict(NCH=self.NCH, NSAMP=self.NSAMP, NDM=self.NDM, IN_PITCH=self.pitch)
+
+    def config_defines(self, cfg: dict) -> dict:
+        return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
+                    TSY=cfg["tile_size_y"], STX=cfg["tile_stride_x"], STY=cfg["tile_stride_y"])
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        grid = (math.ceil(self.NSAMP / (cfg["block_size_x"] * cfg["tile_size_x"])),
+                math.ceil(self.NDM / (cfg["block_size_y"] * cfg["tile_size_y"])), 1)
+        return [Launch(kernel, grid, (cfg["block_size_x"], cfg["block_size_y"], 1),
+                       [_u64(bufs["out"]), _u64(bufs["in"]), C.c_float(self.dm_first),
+                        C.c_float(self.dm_step)])]
+
+    def reference_launches(self, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        return [Launch(kernel, (math.ceil(self.NSAMP / 256), self.NDM, 1), (256, 1, 1),
+                       [_u64(bufs["out"]), _u64(bufs["in"]), C.c_float(self.dm_first),
+                        C.c_float(self.dm_step)])]
+
+    def adds(self) -> float:
+        return float(self.NDM) * self.NSAMP * self.NCH
+
+    def flops(self, cfg=None) -> float:
+        return self.adds()
+
+    def compulsory_bytes(self, cfg=None) -> float:
+        return 4.0 * (self.NCH * self.in_w + self.NDM * self.NSAMP)
+
+    def paper_bytes(self) -> float:
+        """Bytes the kernel *loads* (one fp32 per add): the paper's GB/s basis."""
+        return 4.0 * self.adds()
+
+    def describe(self) -> dict:
+        return {"channels": self.NCH, "samples": self.NSAMP, "dms": self.NDM,
+                "max_shift": self.max_shift, "dtype": "fp32"}
+
+
+# =============================================================================
+# GEMM (CLBlast xgemm space)
+
+
+class Gemm(Problem):
+    """c(m,n) = sum_k a(m,k) b(k,n), BLAS column-major with A transposed:
+    a(m,k) = A[k*M+m], b(k,n) = B[k*N+n], c(m,n) = C[n*M+m]
+    (SURVEY 8a a19 leaves layout unpinned; this is CLBlast's xgemm view).
+    Inputs U[-1,1) (seeds 6, 7).
+    """
+
+    space_name = "gemm"
+    source_file = "gemm.cu"
+    kernel_name = "gemm_kernel"
+    reference_kernel = "gemm_reference"
+
+    def __init__(self, m: int = 4096, n: int = 4096, k: int = 4096, seed_a: int = 6,
+                 seed_b: int = 7):
+        super().__init__()
+        self.M, self.N, self.K = m, n, k
+        self.seed_a, self.seed_b = seed_a, seed_b
+        # identical fmaf chains everywhere -> bit-exact; keep a K-scaled
+        # bound for callers that compare against other orders
+        self.rtol = 1e-5
+
+    def a(self) -> np.ndarray:
+        r = np.random.default_rng(self.seed_a)
+        return (r.random((self.K, self.M), dtype=np.float32) * np.float32(2) - np.float32(1))
+
+    def b(self) -> np.ndarray:
+        r = np.random.default_rng(self.seed_b)
+        return (r.random((self.K, self.N), dtype=np.float32) * np.float32(2) - np.float32(1))
+
+    def host_buffers(self) -> list:
+        return [BufferSpec("A", self.K * self.M * 4, self.a()),
+                BufferSpec("B", self.K * self.N * 4, self.b()),
+                BufferSpec("out", self.M * self.N * 4)]
+
+    @property
+    def output_count(self) -> int:
+        return self.M * self.N
+
+    def problem_defines(self) -> dict:
+        return dict(GM=self.M, GN=self.N, GK=self.K)
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        grid = (self.M // cfg["MWG"], self.N // cfg["NWG"], 1)
+        return [Launch(kernel, grid, (cfg["MDIMC"] * cfg["NDIMC"], 1, 1),
+                       [_u64(bufs["out"]), _u64(bufs["A"]), _u64(bufs["B"])])]
+
+    def reference_launches(self, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        return [Launch(kernel, (math.ceil(self.M / 64), math.ceil(self.N / 4), 1), (256, 1, 1),
+                       [_u64(bufs["out"]), _u64(bufs["A"]), _u64(bufs["B"])])]
+
+    def flops(self, cfg=None) -> float:
+        return 2.0 * self.M * self.N * self.K
+
+    def compulsory_bytes(self, cfg=None) -> float:
+        return 4.0 * (self.M * self.K + self.K * self.N + self.M * self.N)
+
+    def describe(self) -> dict:
+        return {"m": self.M, "n": self.N, "k": self.K, "dtype": "fp32"}
+
+
+PROBLEMS = {"convolution": Convolution, "hotspot": Hotspot, "dedispersion": Dedispersion,
+            "gemm": Gemm}
+
+
+def make_problem(name: str, **kw) -> Problem:
+    try:
+        cls = PROBLEMS[name]
+    except KeyError:
+        raise KeyError(f"unknown problem {name!r}; known: {sorted(PROBLEMS)}") from None
+    return cls(**kw)

@@ -1,0 +1,131 @@
+"""Sweep helpers shared by bench.py, the multi-GPU runner and tools/.
+
+* :func:`stratified_sample` -- deterministic configuration samples
+  (e.g. the hotspot temporal_tiling_factor 1-10 sweep of BASELINE
+  config 1), drawn from the valid flat-index set;
+* :func:`fp32_peak` -- measured FFMA peak of this GPU (roofline
+  denominator for SIMT kernels; MEASURED_PEAKS.json has only HBM/bf16);
+* :func:`roofline` -- algorithmic work of one configuration against the
+  binding B200 ceiling.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import json
+import math
+from pathlib import Path
+
+import numpy as np
+
+from . import runtime as rt
+
+ROOT = Path(__file__).resolve().parent.parent
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback (used only without MEASURED_PEAKS.json)
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "MEASURED_PEAKS.json (driver-measured)",
+                "bf16_tflops": float(d.get("bf16_tflops", 0.0))}
+    return {"hbm_gbs": FALLBACK_HBM_GBS, "source": "B200_PROFILING.md fallback", "bf16_tflops": 1590.0}
+
+
+def stratified_sample(space, n: int, seed: int, param: str | None = None, offset: int = 0) -> list:
+    """``n`` distinct valid configurations, round-robin over ``param``'s values.
+
+    Deterministic in (space, n, seed, param, offset); ``offset`` selects a
+    disjoint block of the same per-stratum permutations (rank / step
+    sharding without overlap).
+    """
+    idx = space.valid_indices()
+    rng = np.random.default_rng(seed)
+    if param is None:
+        perm = rng.permutation(len(idx))
+        take = perm[offset: offset + n]
+        return space.configs_at(idx[take])
+    pi = space.param_names.index(param)
+    configs = space.configs_at(idx)
+    strata: dict = {}
+    for k, c in enumerate(configs):
+        strata.setdefault(c[pi], []).append(k)
+    keys = sorted(strata)
+    perms = {v: rng.permutation(len(strata[v])) for v in keys}
+    out = []
+    per = math.ceil(n / len(keys))
+    start = offset // len(keys)
+    for j in range(per):
+        for v in keys:
+            lst = strata[v]
+            pos = start + j
+            if pos < len(lst) and len(out) < n:
+                out.append(configs[lst[perms[v][pos]]])
+    return out
+
+
+_PEAK_CACHE: dict = {}
+
+
+def fp32_peak(dev: rt.Device, iters: int = 2048) -> dict:
+    """FFMA throughput of this GPU (TFLOP/s), measured with CUDA events."""
+    if dev.index in _PEAK_CACHE:
+        return _PEAK_CACHE[dev.index]
+    src = (Path(__file__).parent / "kernels" / "peak.cu").read_text()
+    res = rt.compile_source(src, ["--gpu-architecture=sm_100a", "-std=c++17"])
+    if not res.ok:
+        raise RuntimeError(res.error)
+    rc, mod = dev.load(res.image)
+    if rc != rt.OK:
+        raise RuntimeError(mod)
+    k = mod.function("ffma_peak")
+    blocks = dev.info["sm_count"] * 8
+    out = dev.alloc(blocks * 256 * 4)
+    launch = rt.Launch(k, (blocks, 1, 1), (256, 1, 1),
+                       [C.c_uint64(out.ptr), C.c_int(iters), C.c_float(0.999), C.c_float(1e-3)])
+    rc, times = dev.run_timed([launch], 2, 5, flush_l2=False)
+    mod.unload()
+    out.free()
+    if rc != rt.OK:
+        raise RuntimeError(times)
+    flop = 2.0 * blocks * 256 * iters * 8 * 16
+    best = min(times)
+    r = {"fp32_tflops": flop / (best * 1e-3) / 1e12, "probe_ms": best,
+         "nominal_tflops_at_max_clock": dev.info["sm_count"] * 128 * 2 * dev.info["clock_khz"] * 1e3 / 1e12}
+    _PEAK_CACHE[dev.index] = r
+    return r
+
+
+def roofline(problem, cfg: dict, info: dict, peaks: dict) -> dict:
+    """Roofline of the dominant launch of one configuration.
+
+    achieved = algorithmic work of that launch / its CUDA-event duration
+    (``info['launch_ms']`` from the last timed run).  The binding bound is
+    the larger of compulsory-HBM time and FP32 time.
+    """
+    launch_ms = info.get("launch_ms") or []
+    if not launch_ms:
+        return {}
+    n = len(launch_ms)
+    dom = int(np.argmax(launch_ms))
+    t = launch_ms[dom] * 1e-3
+    flop = problem.flops(cfg) / n
+    byts = problem.compulsory_bytes(cfg) / n
+    if getattr(problem, "space_name", "") == "hotspot":
+        steps = problem.step_plan(cfg["temporal_tiling_factor"])
+        flop = problem.FLOP_PER_CELL * problem.W * problem.H * steps[dom]
+        byts = 12.0 * problem.W * problem.H
+    hbm_peak = peaks["hbm_gbs"] * 1e9
+    fp32 = peaks.get("fp32_tflops", 0.0) * 1e12
+    t_hbm = byts / hbm_peak
+    t_fp = flop / fp32 if fp32 else 0.0
+    gbs = byts / t / 1e9
+    tfs = flop / t / 1e12
+    if t_hbm >= t_fp:
+        return {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None,
+                "alt": {"fp32_tflops": round(tfs, 3), "fp32_frac": round(tfs * 1e12 / fp32, 4) if fp32 else None}}
+    return {"bound": "fp32", "achieved": round(tfs, 3), "peak": round(fp32 / 1e12, 3), "unit": "TFLOP/s",
+            "frac": round(tfs * 1e12 / fp32, 4), "traffic": None,
+            "alt": {"hbm_gbs": round(gbs, 2), "hbm_frac": round(gbs / peaks["hbm_gbs"], 4)}}

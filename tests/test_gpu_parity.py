@@ -1,0 +1,128 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+* small problems, many configurations per space (stratified, including
+  the extreme block shapes): kernel output BIT-EXACT vs the C oracle;
+* full BASELINE sizes: the on-device answer kernel bit-exact vs the
+  oracle, then a sweep of configurations verified on-device (max
+  relative error stated in the test: 0 expected, 1e-5 tolerated);
+* failure mapping: NVRTC error -> compile_failed, oversize launch ->
+  invalid, never an exception.
+"""
+
+import numpy as np
+import pytest
+
+from oracle import kernels_ffi as K
+from paper_2407_11488_b200.cuda_backend import CudaTarget
+from paper_2407_11488_b200.measure import MeasurementProtocol, Status
+from paper_2407_11488_b200.problems import Convolution, Dedispersion, Gemm, Hotspot
+from paper_2407_11488_b200.sweep import stratified_sample
+
+pytestmark = pytest.mark.gpu
+
+PROTO = MeasurementProtocol(warmup_runs=1, benchmark_runs=2)
+
+SMALL = {
+    "convolution": (lambda: Convolution(width=272, height=200), "tile_size_y", 40),
+    "hotspot": (lambda: Hotspot(width=300, height=260, iterations=20), "temporal_tiling_factor", 60),
+    "dedispersion": (lambda: Dedispersion(channels=48, samples=700, dms=96, dm_step=1.0), "tile_size_y", 40),
+    "gemm": (lambda: Gemm(m=256, n=128, k=96), "VWM", 40),
+}
+
+EDGE = {
+    "convolution": [(16, 1, 1, 1, 0, 0, 0), (256, 4, 4, 4, 1, 0, 0), (16, 16, 4, 4, 1, 1, 1),
+                    (240, 4, 3, 3, 0, 1, 1)],
+    "hotspot": [(1, 32, 1, 1, 1, 1, 0), (1024, 1, 1, 1, 10, 10, 0), (32, 32, 1, 1, 10, 5, 1),
+                (4, 8, 10, 10, 3, 1, 1)],
+    "dedispersion": [(1, 32, 1, 1, 0, 0), (32, 32, 4, 8, 1, 1), (4, 256, 3, 4, 0, 1)],
+    "gemm": [(16, 16, 16, 8, 8, 8, 8, 1, 1, 0, 0, 0, 0), (128, 128, 32, 16, 16, 32, 32, 8, 8, 1, 1, 1, 1),
+             (64, 128, 16, 8, 16, 8, 16, 8, 4, 1, 0, 1, 0)],
+}
+
+
+@pytest.fixture(scope="module")
+def device():
+    from paper_2407_11488_b200 import runtime as rt
+
+    d = rt.Device(0)
+    yield d
+    d.close()
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_small_problem_bit_exact(name, device):
+    make, param, n = SMALL[name]
+    prob = make()
+    want = K.answer(prob)
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        ref = tgt.answer()
+        np.testing.assert_array_equal(ref, want)
+        configs = EDGE[name] + stratified_sample(prob.space, n, seed=11, param=param)
+        ok = 0
+        for c in configs:
+            obs = tgt.execute(c, PROTO)
+            assert obs.status in (Status.OK, Status.INVALID), (c, obs)
+            if not obs.ok:
+                continue
+            st, out = tgt.run_output(c)
+            assert st is Status.OK, (c, out)
+            diff = int(np.sum(out != want))
+            assert diff == 0, f"{name} {c}: {diff} elements differ"
+            ok += 1
+        assert ok >= 0.9 * len(configs)
+    finally:
+        tgt.close()
+
+
+FULL = {"convolution": (Convolution, "tile_size_y", 12), "hotspot": (Hotspot, "temporal_tiling_factor", 20),
+        "dedispersion": (Dedispersion, "tile_size_y", 4), "gemm": (Gemm, "VWM", 6)}
+
+
+@pytest.mark.parametrize("name", sorted(FULL))
+def test_full_size_answer_and_sweep(name, device):
+    cls, param, n = FULL[name]
+    prob = cls()
+    tgt = CudaTarget(prob, device=device)  # answer = naive reference kernel on device
+    try:
+        np.testing.assert_array_equal(tgt.answer(), K.answer(prob))
+        for c in stratified_sample(prob.space, n, seed=5, param=param):
+            obs = tgt.execute(c, PROTO)
+            assert obs.status in (Status.OK, Status.INVALID), (c, obs)
+            if obs.ok:
+                rel = tgt.extras[",".join(map(str, c))]["verify_rel_err"]
+                assert rel <= 1e-5, (c, rel)  # tolerance: 1e-5 norm-wise; bit-exact expected
+                assert rel == 0.0, (c, rel)
+    finally:
+        tgt.close()
+
+
+def test_failure_mapping(device):
+    from paper_2407_11488_b200 import runtime as rt
+
+    bad = rt.compile_source('extern "C" __global__ void k() { nope; }', ["--gpu-architecture=sm_100a"])
+    assert not bad.ok
+    prob = Hotspot(width=64, height=64, iterations=2)
+    tgt = CudaTarget(prob, device=device, answer=K.answer(prob))
+    try:
+        tgt.source = "#error deliberately broken\n" + tgt.source
+        obs = tgt.execute((32, 1, 1, 1, 1, 1, 0), PROTO)
+        assert obs.status is Status.COMPILE_FAILED and "deliberately broken" in obs.detail
+    finally:
+        tgt.close()
+
+
+def test_hotspot_large_smem_configs_run(device):
+    """Configurations needing >48 KiB dynamic smem opt in and verify."""
+    prob = Hotspot(width=512, height=512, iterations=20)
+    want = K.answer(prob)
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        big = [c for c in prob.space.enumerate_configs()
+               if prob.smem_bytes(dict(zip(prob.space.param_names, c))) > 60 * 1024][:5]
+        assert big
+        for c in big:
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+    finally:
+        tgt.close()
