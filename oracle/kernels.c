@@ -129,14 +129,13 @@ static void hotspot_rows(void* p, int y0, int y1) {
       const float s = y < h - 1 ? tin[i + w] : t;
       const float we = x > 0 ? tin[i - 1] : t;
       const float e = x < w - 1 ? tin[i + 1] : t;
-      const float c2 = 2.0f * t;
-      const float ns = (n + s) - c2;
-      const float ew = (e + we) - c2;
-      const float z = amb - t;
-      float d = power[i] + ns * ry1;
-      d = d + ew * rx1;
-      d = d + z * rz1;
-      out[i] = t + sdc * d;
+      /* HS_STEP of kernels/hotspot.cu: explicit fmaf, same order */
+      const float ns = fmaf(-2.0f, t, n + s);
+      const float ew = fmaf(-2.0f, t, e + we);
+      float d = fmaf(ns, ry1, power[i]);
+      d = fmaf(ew, rx1, d);
+      d = fmaf(amb - t, rz1, d);
+      out[i] = fmaf(sdc, d, t);
     }
   }
 }

@@ -1,30 +1,44 @@
 // Hotspot thermal stencil with temporal tiling (paper Table 1 hotspot
 // column; space paper_2407_11488_b200/spaces/hotspot.spec == ref
 // ts/spaces/hotspot.spec:11-25).  Rodinia update, clamped (replicate)
-// boundary:
+// boundary, written with explicit fused multiply-adds:
 //
-//   T' = T + sdc * (P + (N + S - 2T) * ry1 + (E + W - 2T) * rx1 + (amb - T) * rz1)
+//   T' = fma(sdc, fma(amb-T, rz1, fma(fma(-2,T,E+W), rx1, fma(fma(-2,T,N+S), ry1, P))), T)
 //
-// evaluated in exactly this operation order with FMA contraction OFF
-// (compiled with --fmad=false) so every configuration, the naive
-// reference kernel and the CPU oracle (oracle/kernels.c) agree
-// bit-for-bit.  14 FLOP per cell update.
+// (15 FLOP per cell update).  The same operation order is used by every
+// configuration, by the naive reference kernel and by the CPU oracle
+// (oracle/kernels.c), compiled without implicit contraction
+// (--fmad=false), so results agree bit-for-bit.
 //
-// One launch advances the grid by `nsteps` <= TT steps: a block loads
-// its (OH+2TT) x (OW+2TT) window (halo TT on each side) into shared
-// memory, then ping-pongs between two shared buffers, the valid region
-// shrinking by one cell per side per step, and finally writes its
-// OH x OW interior.  Tunables:
-//   BSX, BSY   thread block
-//   TSX, TSY   output cells per thread (OW = BSX*TSX, OH = BSY*TSY)
-//   TT         temporal_tiling_factor (steps fused per launch)
-//   UNROLL     loop_unroll_factor_t (unroll of the time loop)
-//   SH_POWER   stage the power tile in shared memory too
-// Work mapping: thread (tx,ty) owns the window columns tx + i*BSX
-// (coalesced, conflict-free along x) and a CONTIGUOUS run of RY rows,
-// which it sweeps top to bottom keeping N/centre/S in registers, so a
-// cell update costs 3 shared loads (S, E, W) instead of 5.
+// One launch advances the grid by `nsteps` <= TT steps: a block owns an
+// OH x OW output tile plus a halo of TT cells per side (window EH x EW),
+// stages it on chip, advances it nsteps times -- the valid region
+// shrinking by one cell per side per step -- and writes the interior.
+//
+// Tunables: BSX, BSY (block), TSX, TSY (cells per thread: OW = BSX*TSX,
+// OH = BSY*TSY), TT (temporal_tiling_factor), UNROLL
+// (loop_unroll_factor_t, unroll of the time loop), SH_POWER (stage the
+// power tile in shared memory; else re-read it through L1 each step).
+//
+// Thread (tx, ty) owns window columns tx + i*BSX (coalesced, bank-
+// conflict free) and a CONTIGUOUS run of RY rows.  Two schedules,
+// chosen at compile time from the register budget:
+//   REGISTER mode (CX*RY small): the thread's cells live in registers
+//     across all steps; N/S neighbours come from its own registers, only
+//     E/W (and the strip ends) are exchanged through a ping-pong pair of
+//     shared buffers: 2 LDS + 1 STS per cell update, 1 barrier per step.
+//   SHARED mode (large tiles): cells live in the shared ping-pong pair;
+//     each column strip is swept top-down with N/C/S in registers:
+//     3 LDS + 1 STS per cell update.
+// Blocks whose window lies fully inside the grid take a branch-free
+// path; only edge blocks evaluate the clamping selects.
 // Problem macros: GW, GH.
+
+#define HS_STEP(t, n, s, e, w, p, sdc, rx1, ry1, rz1, amb)                              \
+  fmaf((sdc),                                                                            \
+       fmaf((amb) - (t), (rz1),                                                          \
+            fmaf(fmaf(-2.0f, (t), (e) + (w)), (rx1), fmaf(fmaf(-2.0f, (t), (n) + (s)), (ry1), (p)))), \
+       (t))
 
 #ifndef REFERENCE_ONLY
 
@@ -34,27 +48,191 @@
 #define EH (OH + 2 * TT)
 #define CX ((EW + BSX - 1) / BSX)
 #define RY ((EH + BSY - 1) / BSY)
+#define NTHREADS (BSX * BSY)
 
 #define STR2(x) #x
 #define STR(x) STR2(x)
 #define PRAGMA_UNROLL(n) _Pragma(STR(unroll n))
 
-extern "C" __global__ void __launch_bounds__(BSX * BSY)
+// register budget per thread under __launch_bounds__(NTHREADS)
+#define REG_BUDGET ((65536 / NTHREADS) > 255 ? 255 : (65536 / NTHREADS))
+#define REG_CELLS_MAX (((REG_BUDGET - 40) / 2) < 48 ? ((REG_BUDGET - 40) / 2) : 48)
+#if !defined(HS_FORCE_SHARED) && (CX * RY <= REG_CELLS_MAX)
+#define HS_REGISTER_MODE 1
+#else
+#define HS_REGISTER_MODE 0
+#endif
+
+struct HsCoef {
+  float sdc, rx1, ry1, rz1, amb;
+};
+
+#if HS_REGISTER_MODE
+
+template <bool EDGE>
+__device__ __forceinline__ void hs_reg_steps(float (&v)[CX][RY], const float* __restrict__ power,
+                                             float* A, float* B, const float* P, int nsteps,
+                                             int tx, int r0, int gx0, int gy0, HsCoef k) {
+  PRAGMA_UNROLL(UNROLL)
+  for (int s = 0; s < nsteps; ++s) {
+    const int lo = s + 1;
+    float nv[CX][RY];
+#pragma unroll
+    for (int i = 0; i < CX; ++i) {
+      const int c = tx + i * BSX;
+      const int gx = gx0 + c;
+      const bool col_ok = (c >= lo) && (c < EW - lo) && (!EDGE || (gx >= 0 && gx < GW));
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        const int r = r0 + j;
+        const int gy = gy0 + r;
+        nv[i][j] = v[i][j];
+        const bool ok = col_ok && (r >= lo) && (r < EH - lo) && (!EDGE || (gy >= 0 && gy < GH));
+        if (ok) {
+          const float t = v[i][j];
+          float n = (j > 0) ? v[i][j - 1] : A[(r - 1) * EW + c];
+          float so = (j < RY - 1) ? v[i][j + 1] : A[(r + 1) * EW + c];
+          float w = A[r * EW + c - 1];
+          float e = A[r * EW + c + 1];
+          if (EDGE) {
+            n = (gy == 0) ? t : n;
+            so = (gy == GH - 1) ? t : so;
+            w = (gx == 0) ? t : w;
+            e = (gx == GW - 1) ? t : e;
+          }
+#if SH_POWER
+          const float p = P[r * EW + c];
+#else
+          const float p = __ldg(power + (size_t)gy * GW + gx);
+#endif
+          nv[i][j] = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < CX; ++i) {
+      const int c = tx + i * BSX;
+#pragma unroll
+      for (int j = 0; j < RY; ++j) {
+        v[i][j] = nv[i][j];
+        if (c < EW && r0 + j < EH) B[(r0 + j) * EW + c] = nv[i][j];
+      }
+    }
+    __syncthreads();
+    float* tmp = A;
+    A = B;
+    B = tmp;
+  }
+}
+
+#else  // SHARED mode
+
+template <bool EDGE>
+__device__ __forceinline__ float* hs_smem_steps(const float* __restrict__ power, float* A, float* B,
+                                                const float* P, int nsteps, int tx, int r_begin,
+                                                int r_end, int gx0, int gy0, HsCoef k) {
+  PRAGMA_UNROLL(UNROLL)
+  for (int s = 0; s < nsteps; ++s) {
+    const int lo = s + 1;
+    int ra = max(r_begin, lo), rb = min(r_end, EH - lo);
+    if (EDGE) {
+      ra = max(ra, -gy0);
+      rb = min(rb, GH - gy0);
+    }
+#pragma unroll
+    for (int i = 0; i < CX; ++i) {
+      const int c = tx + i * BSX;
+      const int gx = gx0 + c;
+      if (c < lo || c >= EW - lo || ra >= rb) continue;
+      if (EDGE && (gx < 0 || gx >= GW)) continue;
+      const float* a = A + c;
+      float up = a[(ra - 1) * EW];
+      float mid = a[ra * EW];
+      for (int r = ra; r < rb; ++r) {
+        const float dn = a[(r + 1) * EW];
+        const float t = mid;
+        float n = up, so = dn, w = a[r * EW - 1], e = a[r * EW + 1];
+        if (EDGE) {
+          const int gy = gy0 + r;
+          n = (gy == 0) ? t : n;
+          so = (gy == GH - 1) ? t : so;
+          w = (gx == 0) ? t : w;
+          e = (gx == GW - 1) ? t : e;
+        }
+#if SH_POWER
+        const float p = P[r * EW + c];
+#else
+        const float p = __ldg(power + (size_t)(gy0 + r) * GW + gx);
+#endif
+        B[r * EW + c] = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
+        up = mid;
+        mid = dn;
+      }
+    }
+    __syncthreads();
+    float* tmp = A;
+    A = B;
+    B = tmp;
+  }
+  return A;
+}
+
+#endif
+
+extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
                const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
                float rz1, float amb) {
   extern __shared__ float smem[];
   float* A = smem;
   float* B = smem + EH * EW;
-#if SH_POWER
-  float* P = smem + 2 * EH * EW;
-#endif
+  float* P = smem + 2 * EH * EW;  // used only when SH_POWER
+  const HsCoef k{sdc, rx1, ry1, rz1, amb};
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int gx0 = (int)blockIdx.x * OW - TT;
   const int gy0 = (int)blockIdx.y * OH - TT;
   const int r_begin = ty * RY;
   const int r_end = min(r_begin + RY, EH);
+  const bool edge = gx0 < 0 || gy0 < 0 || gx0 + EW > GW || gy0 + EH > GH;
 
+#if HS_REGISTER_MODE
+  float v[CX][RY];
+#pragma unroll
+  for (int i = 0; i < CX; ++i) {
+    const int c = tx + i * BSX;
+    const int gx = gx0 + c;
+#pragma unroll
+    for (int j = 0; j < RY; ++j) {
+      const int r = r_begin + j;
+      const int gy = gy0 + r;
+      v[i][j] = 0.f;
+      if (c < EW && r < EH && gx >= 0 && gx < GW && gy >= 0 && gy < GH) {
+        v[i][j] = __ldg(tin + (size_t)gy * GW + gx);
+#if SH_POWER
+        P[r * EW + c] = __ldg(power + (size_t)gy * GW + gx);
+#endif
+      }
+      if (c < EW && r < EH) A[r * EW + c] = v[i][j];
+    }
+  }
+  __syncthreads();
+  if (edge)
+    hs_reg_steps<true>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
+  else
+    hs_reg_steps<false>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
+#pragma unroll
+  for (int i = 0; i < CX; ++i) {
+    const int c = tx + i * BSX;
+    const int gx = gx0 + c;
+#pragma unroll
+    for (int j = 0; j < RY; ++j) {
+      const int r = r_begin + j;
+      const int gy = gy0 + r;
+      if (c >= TT && c < TT + OW && r >= TT && r < TT + OH && gx < GW && gy < GH)
+        out[(size_t)gy * GW + gx] = v[i][j];
+    }
+  }
+#else
   for (int r = r_begin; r < r_end; ++r) {
     const int gy = gy0 + r;
     if (gy < 0 || gy >= GH) continue;
@@ -71,54 +249,8 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
     }
   }
   __syncthreads();
-
-PRAGMA_UNROLL(UNROLL)
-  for (int s = 0; s < nsteps; ++s) {
-    const int lo = s + 1;
-    const int hi_r = EH - s - 1;
-    const int hi_c = EW - s - 1;
-    const int ra = max(r_begin, max(lo, -gy0));          // first active, in-domain row
-    const int rb = min(r_end, min(hi_r, GH - gy0));      // one past the last
-#pragma unroll
-    for (int i = 0; i < CX; ++i) {
-      const int c = tx + i * BSX;
-      const int gx = gx0 + c;
-      if (c < lo || c >= hi_c || gx < 0 || gx >= GW || ra >= rb) continue;
-      const bool west_edge = (gx == 0), east_edge = (gx == GW - 1);
-      float up = A[(ra - 1) * EW + c];
-      float mid = A[ra * EW + c];
-      for (int r = ra; r < rb; ++r) {
-        const int gy = gy0 + r;
-        const float dn = A[(r + 1) * EW + c];
-        const float t = mid;
-        const float n = (gy == 0) ? t : up;
-        const float so = (gy == GH - 1) ? t : dn;
-        const float w = west_edge ? t : A[r * EW + c - 1];
-        const float e = east_edge ? t : A[r * EW + c + 1];
-#if SH_POWER
-        const float p = P[r * EW + c];
-#else
-        const float p = __ldg(power + (size_t)gy * GW + gx);
-#endif
-        const float c2 = 2.0f * t;
-        const float ns = (n + so) - c2;
-        const float ew = (e + w) - c2;
-        const float z = amb - t;
-        float d = p + ns * ry1;
-        d = d + ew * rx1;
-        d = d + z * rz1;
-        B[r * EW + c] = t + sdc * d;
-        up = mid;
-        mid = dn;
-      }
-    }
-    __syncthreads();
-    float* tmp = A;
-    A = B;
-    B = tmp;
-  }
-
-  // write the OH x OW interior (valid after nsteps <= TT steps)
+  float* R = edge ? hs_smem_steps<true>(power, A, B, P, nsteps, tx, r_begin, r_end, gx0, gy0, k)
+                  : hs_smem_steps<false>(power, A, B, P, nsteps, tx, r_begin, r_end, gx0, gy0, k);
   const int wr0 = max(r_begin, TT), wr1 = min(r_end, TT + OH);
   for (int r = wr0; r < wr1; ++r) {
     const int gy = gy0 + r;
@@ -127,9 +259,10 @@ PRAGMA_UNROLL(UNROLL)
     for (int i = 0; i < CX; ++i) {
       const int c = tx + i * BSX;
       const int gx = gx0 + c;
-      if (c >= TT && c < TT + OW && gx < GW) out[(size_t)gy * GW + gx] = A[r * EW + c];
+      if (c >= TT && c < TT + OW && gx < GW) out[(size_t)gy * GW + gx] = R[r * EW + c];
     }
   }
+#endif
 }
 
 #endif  // REFERENCE_ONLY
@@ -149,12 +282,5 @@ hotspot_reference(float* __restrict__ out, const float* __restrict__ tin,
   const float so = y < GH - 1 ? tin[i + GW] : t;
   const float w = x > 0 ? tin[i - 1] : t;
   const float e = x < GW - 1 ? tin[i + 1] : t;
-  const float c2 = 2.0f * t;
-  const float ns = (n + so) - c2;
-  const float ew = (e + w) - c2;
-  const float z = amb - t;
-  float d = power[i] + ns * ry1;
-  d = d + ew * rx1;
-  d = d + z * rz1;
-  out[i] = t + sdc * d;
+  out[i] = HS_STEP(t, n, so, e, w, power[i], sdc, rx1, ry1, rz1, amb);
 }

@@ -258,7 +258,7 @@ class Hotspot(Problem):
     reference_kernel = "hotspot_reference"
     rtol = 1e-5
     extra_options = ("--fmad=false",)
-    FLOP_PER_CELL = 14
+    FLOP_PER_CELL = 15  # 4 FADD + 5 FMA (kernels/hotspot.cu HS_STEP)
 
     def __init__(self, width: int = 4096, height: int = 4096, iterations: int = 20,
                  seed_temp: int = 3, seed_power: int = 4):

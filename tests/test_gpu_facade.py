@@ -1,0 +1,81 @@
+"""tune_kernel / run_kernel on the GPU (Kernel-Tuner-style facade)."""
+
+import numpy as np
+import pytest
+
+from paper_2407_11488_b200 import run_kernel, tune_kernel
+from paper_2407_11488_b200.paramspace import space_from_tune_params
+from paper_2407_11488_b200.store import import_external_cache
+
+pytestmark = pytest.mark.gpu
+
+VADD = r"""
+extern "C" __global__ void vector_add(float* c, const float* a, const float* b, int n) {
+    int i = blockIdx.x * block_size_x * tile + threadIdx.x;
+    #pragma unroll
+    for (int k = 0; k < tile; ++k, i += block_size_x)
+        if (i < n) c[i] = a[i] + b[i];
+}
+"""
+
+SCALE = r"""
+__constant__ float coef[4];
+template <typename T>
+__global__ void scale(T* out, const T* in, int n) {
+    int i = blockIdx.x * block_size_x + threadIdx.x;
+    if (i < n) out[i] = in[i] * coef[i % 4];
+}
+"""
+
+
+def test_tune_vector_add_with_answer(tmp_path):
+    n = np.int32(1_000_003)
+    a = np.random.default_rng(0).random(n, dtype=np.float32)
+    b = np.random.default_rng(1).random(n, dtype=np.float32)
+    c = np.zeros_like(a)
+    tune_params = {"block_size_x": [64, 128, 256, 512, 1024, 2048], "tile": [1, 2, 4]}
+    cache = tmp_path / "kt.json"
+    results, env = tune_kernel("vector_add", VADD, n, [c, a, b, n], tune_params,
+                               grid_div_x=["block_size_x", "tile"], answer=[a + b, None, None, None],
+                               restrictions=["block_size_x * tile <= 4096"], cache=str(cache),
+                               metrics={"GB/s": lambda p: 12 * n / (p["time"] * 1e6)})
+    assert env["space_size"] == 17 and len(results) == 17
+    ok = [r for r in results if r["status"] == "ok"]
+    bad = [r for r in results if r["status"] != "ok"]
+    assert all(r["block_size_x"] == 2048 for r in bad) and len(bad) == 2  # > 1024 threads
+    assert all(r["status"] == "invalid" for r in bad)
+    assert len(ok) == 15 and all(r["GB/s"] > 0 for r in ok)
+    space = space_from_tune_params("vector_add", tune_params, ["block_size_x * tile <= 4096"])
+    imported = import_external_cache(cache, expected_space=space)
+    assert len(imported.records) == 17
+
+
+def test_wrong_answer_is_runtime_failed():
+    n = np.int32(4096)
+    a = np.ones(n, np.float32)
+    c = np.zeros_like(a)
+    results, _ = tune_kernel("vector_add", VADD, n, [c, a, a, n], {"block_size_x": [128], "tile": [1]},
+                             grid_div_x=["block_size_x", "tile"], answer=[a * 3, None, None, None])
+    assert results[0]["status"] == "runtime_failed" and "verification" in results[0]["error"]
+
+
+def test_run_kernel_template_and_cmem():
+    n = np.int32(1000)
+    x = np.arange(n, dtype=np.float32)
+    out = np.zeros_like(x)
+    coef = np.array([1, 2, 3, 4], np.float32)
+    res = run_kernel("scale<float>", SCALE, n, [out, x, n], {"block_size_x": 128},
+                     cmem_args={"coef": coef})
+    np.testing.assert_array_equal(res[0], x * coef[np.arange(n) % 4])
+
+
+@pytest.mark.parametrize("strategy", ["random_sample", "genetic_algorithm", "greedy_ls"])
+def test_strategies_through_facade(strategy):
+    n = np.int32(1 << 20)
+    a = np.ones(n, np.float32)
+    c = np.zeros_like(a)
+    tp = {"block_size_x": [32, 64, 128, 256, 512, 1024], "tile": [1, 2, 4, 8]}
+    results, env = tune_kernel("vector_add", VADD, n, [c, a, a, n], tp,
+                               grid_div_x=["block_size_x", "tile"], strategy=strategy,
+                               strategy_options={"max_fevals": 8, "seed": 3})
+    assert 1 <= len(results) <= 8 and env["best_config"] is not None

@@ -31,11 +31,11 @@ SMALL = {
 
 EDGE = {
     "convolution": [(16, 1, 1, 1, 0, 0, 0), (256, 4, 4, 4, 1, 0, 0), (16, 16, 4, 4, 1, 1, 1),
-                    (240, 4, 3, 3, 0, 1, 1)],
-    "hotspot": [(1, 32, 1, 1, 1, 1, 0), (1024, 1, 1, 1, 10, 10, 0), (32, 32, 1, 1, 10, 5, 1),
+                    (240, 1, 3, 2, 0, 1, 1)],
+    "hotspot": [(1, 32, 1, 1, 1, 1, 0), (1024, 1, 1, 1, 1, 1, 0), (32, 32, 1, 1, 10, 5, 1),
                 (4, 8, 10, 10, 3, 1, 1)],
     "dedispersion": [(1, 32, 1, 1, 0, 0), (32, 32, 4, 8, 1, 1), (4, 256, 3, 4, 0, 1)],
-    "gemm": [(16, 16, 16, 8, 8, 8, 8, 1, 1, 0, 0, 0, 0), (128, 128, 32, 16, 16, 32, 32, 8, 8, 1, 1, 1, 1),
+    "gemm": [(16, 16, 16, 8, 8, 8, 8, 1, 1, 0, 0, 0, 0), (128, 128, 32, 16, 16, 16, 16, 8, 8, 1, 1, 1, 1),
              (64, 128, 16, 8, 16, 8, 16, 8, 4, 1, 0, 1, 0)],
 }
 
@@ -59,6 +59,7 @@ def test_small_problem_bit_exact(name, device):
         ref = tgt.answer()
         np.testing.assert_array_equal(ref, want)
         configs = EDGE[name] + stratified_sample(prob.space, n, seed=11, param=param)
+        assert all(prob.space.is_valid(c) for c in configs)
         ok = 0
         for c in configs:
             obs = tgt.execute(c, PROTO)
