@@ -56,11 +56,27 @@
 
 // register budget per thread under __launch_bounds__(NTHREADS)
 #define REG_BUDGET ((65536 / NTHREADS) > 255 ? 255 : (65536 / NTHREADS))
-#define REG_CELLS_MAX (((REG_BUDGET - 40) / 2) < 48 ? ((REG_BUDGET - 40) / 2) : 48)
-#if !defined(HS_FORCE_SHARED) && (CX * RY <= REG_CELLS_MAX)
+#define REG_CELLS_MAX (((REG_BUDGET - 40) / 2) < 32 ? ((REG_BUDGET - 40) / 2) : 32)
+// padded window of register mode: row pitch SP, RT rows; each thread-row
+// strip of RY rows starts SS floats after the previous one, SS = RY*SP +
+// a skew chosen so that the 32/BSX thread rows sharing a warp land on
+// disjoint bank groups (SS = BSX * odd (mod 32)) -- no bank conflicts.
+#define SP (CX * BSX)
+#define RT (RY * BSY)
+#define SKEW_M (2 * BSX)
+#define SKEW ((BSX >= 32) ? 0 : ((BSX - ((RY * SP) % SKEW_M) + SKEW_M) % SKEW_M))
+#define SS (RY * SP + SKEW)
+#define REG_GUARD (SP + 33)
+#define REG_SMEM_BYTES (4 * ((2 + SH_POWER) * BSY * SS + 3 * REG_GUARD))
+// (mirrored on the host by problems.Hotspot.kernel_mode / smem_bytes)
+#if !defined(HS_FORCE_SHARED) && (CX * RY <= REG_CELLS_MAX) && (REG_SMEM_BYTES <= 200 * 1024)
 #define HS_REGISTER_MODE 1
+#define HS_BUF (BSY * SS)
+#define HS_GUARD REG_GUARD
 #else
 #define HS_REGISTER_MODE 0
+#define HS_BUF (EH * EW)
+#define HS_GUARD (EW + 1)
 #endif
 
 struct HsCoef {
@@ -69,55 +85,80 @@ struct HsCoef {
 
 #if HS_REGISTER_MODE
 
+// Register mode works on a PADDED window: row pitch SP = CX*BSX and RT =
+// RY*BSY rows, so every thread cell (i, j) has its own smem slot at the
+// affine index tb + j*SP + i*BSX (compile-time offsets from one per-thread
+// base).  Cells are computed branch-free; activity (the shrinking valid
+// region, domain edges) is one select per cell from per-row / per-column
+// predicates evaluated once per step, and rows with no active cell in the
+// warp are skipped with a warp-uniform test.  Guard bands of SP+1 floats
+// before/after each buffer keep the +-1 / +-SP reads of border cells in
+// bounds; those values only ever feed inactive (discarded) cells.
 template <bool EDGE>
 __device__ __forceinline__ void hs_reg_steps(float (&v)[CX][RY], const float* __restrict__ power,
                                              float* A, float* B, const float* P, int nsteps,
                                              int tx, int r0, int gx0, int gy0, HsCoef k) {
+  const int tb = (r0 / RY) * SS + tx;  // strip of thread row r0/RY
   PRAGMA_UNROLL(UNROLL)
   for (int s = 0; s < nsteps; ++s) {
     const int lo = s + 1;
     float nv[CX][RY];
+    bool col_ok[CX];
 #pragma unroll
     for (int i = 0; i < CX; ++i) {
       const int c = tx + i * BSX;
-      const int gx = gx0 + c;
-      const bool col_ok = (c >= lo) && (c < EW - lo) && (!EDGE || (gx >= 0 && gx < GW));
+      col_ok[i] = (c >= lo) && (c < EW - lo);
+      if (EDGE) col_ok[i] = col_ok[i] && (gx0 + c >= 0) && (gx0 + c < GW);
+    }
 #pragma unroll
-      for (int j = 0; j < RY; ++j) {
-        const int r = r0 + j;
-        const int gy = gy0 + r;
-        nv[i][j] = v[i][j];
-        const bool ok = col_ok && (r >= lo) && (r < EH - lo) && (!EDGE || (gy >= 0 && gy < GH));
-        if (ok) {
+    for (int j = 0; j < RY; ++j) {
+      const int r = r0 + j;
+      bool row_ok = (r >= lo) && (r < EH - lo);
+      if (EDGE) row_ok = row_ok && (gy0 + r >= 0) && (gy0 + r < GH);
+      float* bj = B + tb + j * SP;
+      if (__any_sync(0xffffffffu, row_ok)) {
+        const float* aj = A + tb + j * SP;
+#pragma unroll
+        for (int i = 0; i < CX; ++i) {
           const float t = v[i][j];
-          float n = (j > 0) ? v[i][j - 1] : A[(r - 1) * EW + c];
-          float so = (j < RY - 1) ? v[i][j + 1] : A[(r + 1) * EW + c];
-          float w = A[r * EW + c - 1];
-          float e = A[r * EW + c + 1];
+          // strip ends: the neighbour row lives in the adjacent strip
+          float n = (j > 0) ? v[i][j - 1] : aj[i * BSX + (RY - 1) * SP - SS];
+          float so = (j < RY - 1) ? v[i][j + 1] : aj[i * BSX + SS - (RY - 1) * SP];
+          float w = aj[i * BSX - 1];
+          float e = aj[i * BSX + 1];
           if (EDGE) {
+            const int gx = gx0 + tx + i * BSX, gy = gy0 + r;
             n = (gy == 0) ? t : n;
             so = (gy == GH - 1) ? t : so;
             w = (gx == 0) ? t : w;
             e = (gx == GW - 1) ? t : e;
           }
 #if SH_POWER
-          const float p = P[r * EW + c];
+          const float p = P[tb + j * SP + i * BSX];
 #else
-          const float p = __ldg(power + (size_t)gy * GW + gx);
+          int gyp = gy0 + r, gxp = gx0 + tx + i * BSX;
+          if (EDGE) {
+            gyp = min(max(gyp, 0), GH - 1);
+            gxp = min(max(gxp, 0), GW - 1);
+          }
+          const float p = __ldg(power + (size_t)gyp * GW + gxp);
 #endif
-          nv[i][j] = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
+          const float u = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
+          nv[i][j] = (row_ok && col_ok[i]) ? u : t;
+          bj[i * BSX] = nv[i][j];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < CX; ++i) {
+          nv[i][j] = v[i][j];
+          bj[i * BSX] = v[i][j];
         }
       }
     }
 #pragma unroll
-    for (int i = 0; i < CX; ++i) {
-      const int c = tx + i * BSX;
+    for (int i = 0; i < CX; ++i)
 #pragma unroll
-      for (int j = 0; j < RY; ++j) {
-        v[i][j] = nv[i][j];
-        if (c < EW && r0 + j < EH) B[(r0 + j) * EW + c] = nv[i][j];
-      }
-    }
+      for (int j = 0; j < RY; ++j) v[i][j] = nv[i][j];
     __syncthreads();
     float* tmp = A;
     A = B;
@@ -184,9 +225,11 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
                const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
                float rz1, float amb) {
   extern __shared__ float smem[];
-  float* A = smem;
-  float* B = smem + EH * EW;
-  float* P = smem + 2 * EH * EW;  // used only when SH_POWER
+  // [guard][A][guard][B][guard][P], each buffer HS_BUF floats; the guards
+  // absorb register mode's one-row/one-column overreach at the borders
+  float* A = smem + HS_GUARD;
+  float* B = A + HS_BUF + HS_GUARD;
+  float* P = B + HS_BUF + HS_GUARD;  // used only when SH_POWER
   const HsCoef k{sdc, rx1, ry1, rz1, amb};
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int gx0 = (int)blockIdx.x * OW - TT;
@@ -196,30 +239,33 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   const bool edge = gx0 < 0 || gy0 < 0 || gx0 + EW > GW || gy0 + EH > GH;
 
 #if HS_REGISTER_MODE
+  // interior: the whole PADDED window maps inside the grid (padding cells
+  // then read valid global addresses and need no clamping)
+  const bool interior = gx0 >= 0 && gy0 >= 0 && gx0 + SP <= GW && gy0 + RT <= GH;
   float v[CX][RY];
+  const int tb = ty * SS + tx;
 #pragma unroll
   for (int i = 0; i < CX; ++i) {
     const int c = tx + i * BSX;
     const int gx = gx0 + c;
 #pragma unroll
     for (int j = 0; j < RY; ++j) {
-      const int r = r_begin + j;
-      const int gy = gy0 + r;
+      const int gy = gy0 + r_begin + j;
       v[i][j] = 0.f;
-      if (c < EW && r < EH && gx >= 0 && gx < GW && gy >= 0 && gy < GH) {
+      if (interior || (gx >= 0 && gx < GW && gy >= 0 && gy < GH)) {
         v[i][j] = __ldg(tin + (size_t)gy * GW + gx);
 #if SH_POWER
-        P[r * EW + c] = __ldg(power + (size_t)gy * GW + gx);
+        P[tb + j * SP + i * BSX] = __ldg(power + (size_t)gy * GW + gx);
 #endif
       }
-      if (c < EW && r < EH) A[r * EW + c] = v[i][j];
+      A[tb + j * SP + i * BSX] = v[i][j];
     }
   }
   __syncthreads();
-  if (edge)
-    hs_reg_steps<true>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
-  else
+  if (interior)
     hs_reg_steps<false>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
+  else
+    hs_reg_steps<true>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
 #pragma unroll
   for (int i = 0; i < CX; ++i) {
     const int c = tx + i * BSX;

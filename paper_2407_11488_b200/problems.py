@@ -292,11 +292,31 @@ class Hotspot(Problem):
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
                     UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"])
 
+    @staticmethod
+    def kernel_mode(cfg: dict) -> tuple:
+        """(mode, floats per buffer, guard floats) -- mirrors kernels/hotspot.cu macros."""
+        bx, by = cfg["block_size_x"], cfg["block_size_y"]
+        t, shp = cfg["temporal_tiling_factor"], cfg["sh_power"]
+        ew = bx * cfg["tile_size_x"] + 2 * t
+        eh = by * cfg["tile_size_y"] + 2 * t
+        cx, ry = -(-ew // bx), -(-eh // by)
+        budget = min(255, 65536 // (bx * by))
+        cells_max = min(32, (budget - 40) // 2)
+        sp = cx * bx
+        skew = 0 if bx >= 32 else (bx - (ry * sp) % (2 * bx)) % (2 * bx)
+        ss = ry * sp + skew
+        guard = sp + 33
+        reg_bytes = 4 * ((2 + shp) * by * ss + 3 * guard)
+        if cx * ry <= cells_max and reg_bytes <= 200 * 1024:
+            return "register", by * ss, guard
+        return "shared", eh * ew, ew + 1
+
     def smem_bytes(self, cfg: dict) -> int:
-        t = cfg["temporal_tiling_factor"]
-        ew = cfg["block_size_x"] * cfg["tile_size_x"] + 2 * t
-        eh = cfg["block_size_y"] * cfg["tile_size_y"] + 2 * t
-        return (2 + cfg["sh_power"]) * ew * eh * 4
+        # (2 + sh_power) window buffers (the space's own smem model,
+        # ts/spaces/hotspot.spec:25; register mode pads rows/columns to the
+        # thread grid) + three pitch+1 guard bands
+        _, buf, guard = self.kernel_mode(cfg)
+        return 4 * ((2 + cfg["sh_power"]) * buf + 3 * guard)
 
     def step_plan(self, t: int) -> list:
         n = math.ceil(self.iterations / t)

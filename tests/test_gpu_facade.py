@@ -79,3 +79,19 @@ def test_strategies_through_facade(strategy):
                                grid_div_x=["block_size_x", "tile"], strategy=strategy,
                                strategy_options={"max_fevals": 8, "seed": 3})
     assert 1 <= len(results) <= 8 and env["best_config"] is not None
+
+
+def test_tsbench_through_command_backend():
+    """The reference's cmd: route (same stdout contract) drives B200 kernels."""
+    import sys
+
+    from paper_2407_11488_b200.measure import MeasurementProtocol, command_backend, measure
+    from paper_2407_11488_b200.paramspace import bundled_space
+
+    space = bundled_space("hotspot")
+    tpl = (f"{sys.executable} -m paper_2407_11488_b200.tsbench --kernel hotspot --size width=512,height=512 "
+           "--config {block_size_x},{block_size_y},{tile_size_x},{tile_size_y},"
+           "{temporal_tiling_factor},{loop_unroll_factor_t},{sh_power}")
+    be = command_backend(tpl)
+    obs = measure(be, (32, 8, 2, 2, 5, 5, 1), MeasurementProtocol(), space.param_names)
+    assert obs.ok and len(obs.times_ms) == 7, obs

@@ -1,0 +1,99 @@
+"""Config sharding across ranks (world_size 2, gloo, CPU).
+
+Each rank replays a recorded cache (the reference's simulated backend as
+the fake GPU) and pulls chunks from the shared TCPStore
+queue; the merged result must equal the single-process brute force:
+same trace order, same best, byte-identical canonical cache.
+"""
+
+import os
+import random
+import socket
+
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2407_11488_b200.measure import MeasurementProtocol, Observation, Status, simulated_backend
+from paper_2407_11488_b200.multigpu import ChunkQueue, sharded_brute_force, torch_dist_plumbing
+from paper_2407_11488_b200.paramspace import bundled_space, config_key
+from paper_2407_11488_b200.store import TuningCache, dumps_cache
+from paper_2407_11488_b200.strategies import brute_force
+
+
+def make_cache(space, seed=0):
+    rng = random.Random(seed)
+    recs = {}
+    for c in space.enumerate_configs():
+        if rng.random() < 0.05:
+            recs[config_key(c)] = Observation(Status.INVALID)
+        else:
+            t = round(rng.uniform(0.1, 50.0), 6)
+            recs[config_key(c)] = Observation(Status.OK, (t,), t, space.metric_value(t, c))
+    return TuningCache(space.kernel_name, "devA", space.param_names, recs, space.fingerprint())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        space = bundled_space("convolution")
+        be = simulated_backend(make_cache(space))
+        store, gather, r, w = torch_dist_plumbing()
+        assert (r, w) == (rank, world)
+        res, cache, stats = sharded_brute_force(space, be, MeasurementProtocol(), chunk=37, store=store,
+                                                gather=gather, rank=rank, device_name="devA")
+        with open(os.path.join(outdir, f"rank{rank}.txt"), "w") as f:
+            f.write(dumps_cache(cache))
+            f.write(f"BEST {config_key(res.best)}\n")
+            f.write(f"MINE {stats[rank].configs}\n")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_sweep_matches_single_process(tmp_path):
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    space = bundled_space("convolution")
+    be = simulated_backend(make_cache(space))
+    res, cache = brute_force(space, be, MeasurementProtocol(), device_name="devA")
+    want = dumps_cache(cache) + f"BEST {config_key(res.best)}\n"
+    shares = []
+    for r in range(world):
+        text = (tmp_path / f"rank{r}.txt").read_text()
+        body, mine = text.rsplit("MINE ", 1)
+        assert body == want
+        shares.append(int(mine))
+    assert sum(shares) == space.space_size() and min(shares) > 0
+
+
+def test_chunk_queue_local():
+    q = ChunkQueue(10, 4)
+    assert [q.next(), q.next(), q.next(), q.next()] == [(0, 4), (4, 8), (8, 10), None]
+
+
+def test_resume_from_log(tmp_path):
+    space = bundled_space("dedispersion")
+    be = simulated_backend(make_cache(space, seed=3))
+    log = tmp_path / "log.jsonl"
+    configs = list(space.enumerate_configs())[:100]
+    r1, c1, _ = sharded_brute_force(space, be, MeasurementProtocol(), log_path=str(log), configs=configs)
+    lines = log.read_text().splitlines()
+    assert len(lines) == 100
+    # a torn final line and a rerun: nothing is re-measured, result identical
+    log.write_text("\n".join(lines[:60]) + "\n{\"key\": \"broken")
+    r2, c2, _ = sharded_brute_force(space, be, MeasurementProtocol(), log_path=str(log), configs=configs)
+    assert dumps_cache(c1) == dumps_cache(c2)
+    # the log is whole again: a third run measures nothing new
+    from paper_2407_11488_b200.store import ResultLog
+
+    assert len(ResultLog(log).load()) == 100
