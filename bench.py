@@ -54,6 +54,7 @@ WORKLOADS = {
     "dedispersion": dict(param="tile_size_y", batch=8,
                          desc="dedispersion 1536 ch x 2048 DM x 25000 samples fp32"),
     "gemm": dict(param="VWM", batch=12, desc="gemm 4096^3 fp32 CLBlast space"),
+    "gemm_tc": dict(param=None, batch=8, desc="gemm 4096^3 tf32 tcgen05/TMEM/TMA variant (BN_T x STAGES)"),
 }
 
 

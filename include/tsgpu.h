@@ -150,6 +150,14 @@ int tsg_run_timed(tsg_ctx* ctx, const tsg_launch_t* seq, int n_launch, int warmu
  * roofline accounting of the dominant kernel. */
 int tsg_last_launch_times(tsg_ctx* ctx, float* times_ms, int n_launch);
 
+/* TMA: encode a 2-D fp32 tensor map (CUtensorMap, 128 bytes written to
+ * `desc128`) for `cp.async.bulk.tensor` in kernels that take it as a
+ * __grid_constant__ parameter.  dim0 is contiguous; stride1_bytes is the
+ * byte pitch of dim1; box0 x box1 elements per copy; swizzle_bytes in
+ * {0, 32, 64, 128}. */
+int tsg_tma_encode_2d_f32(tsg_ctx* ctx, void* desc128, uint64_t gaddr, uint64_t dim0, uint64_t dim1,
+                          uint64_t stride1_bytes, uint32_t box0, uint32_t box1, int swizzle_bytes);
+
 /* Stream markers for timing a whole region (e.g. one benchmark step of
  * many configurations) on the context's stream: record event `slot`
  * (0..15), then read the device time between two recorded slots (waits

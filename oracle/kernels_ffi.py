@@ -98,7 +98,7 @@ def gemm(prob) -> np.ndarray:
 
 def answer(prob) -> np.ndarray:
     return {"convolution": convolution, "hotspot": hotspot, "dedispersion": dedispersion,
-            "gemm": gemm}[prob.space_name](prob)
+            "gemm": gemm, "gemm_tc": gemm}[prob.space_name](prob)
 
 
 # ---------------------------------------------------------------------------

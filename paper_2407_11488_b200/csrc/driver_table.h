@@ -42,6 +42,7 @@
   X(cuStreamCreate) \
   X(cuStreamDestroy) \
   X(cuStreamSynchronize) \
+  X(cuTensorMapEncodeTiled) \
 
 struct TsgDriver {
 #define TSG_DECL(f) decltype(&f) p_##f = nullptr;
@@ -145,3 +146,5 @@ inline const char* tsg_load_driver() {
 #define cuStreamDestroy (tsg_drv().p_cuStreamDestroy)
 #undef cuStreamSynchronize
 #define cuStreamSynchronize (tsg_drv().p_cuStreamSynchronize)
+#undef cuTensorMapEncodeTiled
+#define cuTensorMapEncodeTiled (tsg_drv().p_cuTensorMapEncodeTiled)

@@ -549,6 +549,31 @@ int tsg_run_timed(tsg_ctx* c, const tsg_launch_t* seq, int n, int warmup, int ru
   return TSG_OK;
 }
 
+int tsg_tma_encode_2d_f32(tsg_ctx* c, void* desc128, uint64_t gaddr, uint64_t dim0, uint64_t dim1,
+                          uint64_t stride1_bytes, uint32_t box0, uint32_t box1, int swizzle_bytes) {
+  int s = make_current(c);
+  if (s) return s;
+  if (!desc128) return fail(TSG_ERR_ARG, "null descriptor buffer");
+  CUtensorMapSwizzle sw;
+  switch (swizzle_bytes) {
+    case 0: sw = CU_TENSOR_MAP_SWIZZLE_NONE; break;
+    case 32: sw = CU_TENSOR_MAP_SWIZZLE_32B; break;
+    case 64: sw = CU_TENSOR_MAP_SWIZZLE_64B; break;
+    case 128: sw = CU_TENSOR_MAP_SWIZZLE_128B; break;
+    default: return fail(TSG_ERR_ARG, "swizzle must be 0/32/64/128");
+  }
+  cuuint64_t dims[2] = {dim0, dim1};
+  cuuint64_t strides[1] = {stride1_bytes};
+  cuuint32_t box[2] = {box0, box1};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = cuTensorMapEncodeTiled(reinterpret_cast<CUtensorMap*>(desc128), CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      reinterpret_cast<void*>(gaddr), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(TSG_ERR_INVALID, "cuTensorMapEncodeTiled: " + cu_msg(r));
+  return TSG_OK;
+}
+
 int tsg_event_record(tsg_ctx* c, int slot) {
   int s = make_current(c);
   if (s) return s;

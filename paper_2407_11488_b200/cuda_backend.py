@@ -232,7 +232,9 @@ class CudaTarget:
                 rel = cmp["max_abs_err"] / cmp["max_abs_ref"] if cmp["max_abs_ref"] > 0 else \
                     cmp["max_abs_err"]
                 info["verify_rel_err"] = rel
-                if cmp["n_nonfinite"] or rel > self.problem.rtol:
+                abs_tol = getattr(self.problem, "abs_tol", None)
+                bad = (cmp["max_abs_err"] > abs_tol) if abs_tol is not None else (rel > self.problem.rtol)
+                if cmp["n_nonfinite"] or bad:
                     self.stats["verify_failed"] += 1
                     return Observation(
                         Status.RUNTIME_FAILED,

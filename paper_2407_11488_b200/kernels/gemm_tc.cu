@@ -1,0 +1,210 @@
+// TF32 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA),
+// the north_star's optional B200 variant of the CLBlast GEMM.  Same data
+// layout as kernels/gemm.cu (BLAS column-major with A transposed):
+//
+//   a(m,k) = A[k*GM + m]   b(k,n) = B[k*GN + n]   c(m,n) = C[n*GM + m]
+//
+// so both operands are MN-major in global memory and are consumed as
+// MN-major UMMA operands directly (no transpose pass).
+//
+// One CTA computes a BM x BN = 128 x BN_T tile (BN_T in {128, 256}):
+//   warp 0      TMA producer: per k-block of BK=32, (BM/32) A boxes and
+//               (BN_T/32) B boxes of 32(MN) x 32(K) fp32, 128B swizzle,
+//               into a STAGES-deep ring guarded by full/empty mbarriers
+//   warp 1      TMEM allocator + single-thread MMA issuer:
+//               tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN_T, K=8,
+//               4 per k-block, accumulator in TMEM (BN_T fp32 columns);
+//               tcgen05.commit frees the smem stage / signals the epilogue
+//   warps 2-5   epilogue: tcgen05.ld 32x32b (TMEM lane = m) -> registers
+//               -> coalesced column stores of C (m contiguous)
+// Tunables (compile-time): BN_T, STAGES.  Problem macros: GM, GN, GK.
+// Precision: operands are read as TF32 (10-bit mantissa) by the tensor
+// core, accumulation is fp32; verification uses a K-scaled tolerance.
+
+#ifndef BN_T
+#define BN_T 256
+#endif
+#ifndef STAGES
+#define STAGES 4
+#endif
+#define BM 128
+#define BK 32
+#define KSTEP 8
+#define A_BOXES (BM / 32)
+#define B_BOXES (BN_T / 32)
+#define BOX_BYTES (32 * 32 * 4)
+#define A_STAGE_BYTES (A_BOXES * BOX_BYTES)
+#define B_STAGE_BYTES (B_BOXES * BOX_BYTES)
+#define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
+#define NUM_THREADS 192
+#define TMEM_COLS BN_T
+
+struct __align__(64) TmaDesc {
+  unsigned long long v[16];
+};
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(unsigned dst, const TmaDesc* desc, int c0, int c1, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(desc)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+
+// UMMA shared-memory descriptor, MN-major, 128B swizzle (canonical
+// ((8,n),(8,k)) in 16-byte units: LBO = MN-block stride, SBO = 8-row K stride)
+__device__ __forceinline__ unsigned long long umma_desc(unsigned addr, unsigned lbo, unsigned sbo) {
+  unsigned long long d = 0;
+  d |= (unsigned long long)((addr >> 4) & 0x3FFF);
+  d |= (unsigned long long)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (unsigned long long)((sbo >> 4) & 0x3FFF) << 32;
+  d |= 1ull << 46;  // descriptor version (Blackwell)
+  d |= 2ull << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D=f32, A=B=tf32, A and B MN-major, N=BN_T, M=128
+#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | \
+               ((unsigned)(BN_T >> 3) << 17) | ((unsigned)(BM >> 4) << 24))
+
+__device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db,
+                                          unsigned accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(unsigned bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
+gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
+               const __grid_constant__ TmaDesc tma_b) {
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte alignment for the 128B-swizzle atoms
+  const unsigned base = smem_u32(smem_raw);
+  const unsigned pad = (1024u - (base & 1023u)) & 1023u;
+  unsigned char* smem = smem_raw + pad;
+  const unsigned sbase = base + pad;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * STAGES + 1);
+  const unsigned full0 = smem_u32(bars);
+  const unsigned empty0 = full0 + 8 * STAGES;
+  const unsigned tfull = full0 + 16 * STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN_T;
+  constexpr int KB = GK / BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tma_a)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tma_b)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const unsigned tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned ph = (kb / STAGES) & 1;
+        mbar_wait(empty0 + 8 * s, ph ^ 1);
+        const unsigned full = full0 + 8 * s;
+        mbar_expect_tx(full, STAGE_BYTES);
+        const unsigned sa = sbase + s * STAGE_BYTES;
+        const unsigned sb = sa + A_STAGE_BYTES;
+#pragma unroll
+        for (int i = 0; i < A_BOXES; ++i) tma_load_2d(sa + i * BOX_BYTES, &tma_a, m0 + 32 * i, kb * BK, full);
+#pragma unroll
+        for (int i = 0; i < B_BOXES; ++i) tma_load_2d(sb + i * BOX_BYTES, &tma_b, n0 + 32 * i, kb * BK, full);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer (single thread)
+      for (int kb = 0; kb < KB; ++kb) {
+        const int s = kb % STAGES;
+        const unsigned ph = (kb / STAGES) & 1;
+        mbar_wait(full0 + 8 * s, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const unsigned sa = sbase + s * STAGE_BYTES;
+        const unsigned sb = sa + A_STAGE_BYTES;
+#pragma unroll
+        for (int k = 0; k < BK / KSTEP; ++k) {
+          // K step of 8 rows = one 1024-byte swizzle atom down each MN block
+          const unsigned long long da = umma_desc(sa + k * 1024, BOX_BYTES, 1024);
+          const unsigned long long db = umma_desc(sb + k * 1024, BOX_BYTES, 1024);
+          umma_tf32(tmem, da, db, (kb | k) != 0);
+        }
+        umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs retire
+      }
+      umma_commit(tfull);  // accumulator complete
+    }
+  } else {
+    // ---- epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int m = m0 + q * 32 + lane;
+    const unsigned taddr = tmem + ((unsigned)(q * 32) << 16);
+#pragma unroll 1
+    for (int c = 0; c < BN_T; c += 16) {
+      unsigned r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr + c));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+      for (int j = 0; j < 16; ++j) C[(size_t)(n0 + c + j) * GM + m] = __uint_as_float(r[j]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+// smem bytes the host must request
+#define GEMM_TC_SMEM (STAGES * STAGE_BYTES + 1024 + 256)

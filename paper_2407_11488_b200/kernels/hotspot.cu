@@ -236,7 +236,6 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   const int gy0 = (int)blockIdx.y * OH - TT;
   const int r_begin = ty * RY;
   const int r_end = min(r_begin + RY, EH);
-  const bool edge = gx0 < 0 || gy0 < 0 || gx0 + EW > GW || gy0 + EH > GH;
 
 #if HS_REGISTER_MODE
   // interior: the whole PADDED window maps inside the grid (padding cells
@@ -295,6 +294,7 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
     }
   }
   __syncthreads();
+  const bool edge = gx0 < 0 || gy0 < 0 || gx0 + EW > GW || gy0 + EH > GH;
   float* R = edge ? hs_smem_steps<true>(power, A, B, P, nsteps, tx, r_begin, r_end, gx0, gy0, k)
                   : hs_smem_steps<false>(power, A, B, P, nsteps, tx, r_begin, r_end, gx0, gy0, k);
   const int wr0 = max(r_begin, TT), wr1 = min(r_end, TT + OH);

@@ -51,6 +51,7 @@ class Problem:
     reference_kernel: str = ""
     rtol: float = 1e-5
     atol: float = 0.0
+    abs_tol: float | None = None  # when set: pass iff max|out-ref| <= abs_tol
     extra_options: tuple = ()
 
     def __init__(self):
@@ -547,8 +548,58 @@ class Gemm(Problem):
         return {"m": self.M, "n": self.N, "k": self.K, "dtype": "fp32"}
 
 
+class GemmTC(Gemm):
+    """The tf32 tcgen05/TMEM/TMA variant of :class:`Gemm` (same layout).
+
+    Not part of the reference's GEMM space (north_star: "optional ...
+    variant"), so it carries its own small space: the N extent of the
+    UMMA tile (BN_T) and the smem pipeline depth (STAGES), restricted to
+    B200's 227 KB of shared memory per CTA.  Verified against the fp32
+    naive kernel with a K-scaled tf32 tolerance: max|dC| <= K * 2^-11 *
+    max|a|*max|b| relative to max|C| (= 2/max|C| here, ~0.02).
+    """
+
+    space_name = "gemm_tc"
+    source_file = "gemm_tc.cu"
+    kernel_name = "gemm_tc_kernel"
+    reference_kernel = "gemm_reference"
+
+    def __init__(self, m: int = 4096, n: int = 4096, k: int = 4096, seed_a: int = 6, seed_b: int = 7):
+        from .paramspace import space_from_tune_params
+
+        self.space = space_from_tune_params(
+            "gemm_tc", {"BN_T": [128, 256], "STAGES": [2, 3, 4, 5, 6]},
+            ["STAGES * (16384 + BN_T * 128) + 1280 <= 232448"],
+            metric="(2 * 4096^3) / (time_ms * 1e6)")
+        self._host = None
+        self.M, self.N, self.K = m, n, k
+        self.seed_a, self.seed_b = seed_a, seed_b
+        # K-scaled tf32 bound (SURVEY 8c): |dC| <= c*K*eps*max|a|*max|b|, eps = 2^-11, c = 1
+        self.abs_tol = self.K * 2.0 ** -11
+        self.rtol = 1.0  # the norm-wise check is replaced by abs_tol
+
+    def source(self) -> str:
+        # the fp32 naive answer kernel comes from gemm.cu (tuned part compiled out)
+        return _src("gemm_tc.cu") + "\n#undef REFERENCE_ONLY\n#define REFERENCE_ONLY 1\n" + _src("gemm.cu")
+
+    def config_defines(self, cfg: dict) -> dict:
+        return {"BN_T": cfg["BN_T"], "STAGES": cfg["STAGES"]}
+
+    def smem_bytes(self, cfg: dict) -> int:
+        return cfg["STAGES"] * (16384 + cfg["BN_T"] * 128) + 1024 + 256
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        from .runtime import Launch
+
+        dev = bufs["A"].dev
+        ta = dev.tma_2d_f32(bufs["A"], self.M, self.K, self.M * 4, 32, 32, 128)
+        tb = dev.tma_2d_f32(bufs["B"], self.N, self.K, self.N * 4, 32, 32, 128)
+        grid = (self.M // 128, self.N // cfg["BN_T"], 1)
+        return [Launch(kernel, grid, (192, 1, 1), [_u64(bufs["out"]), ta, tb], smem=self.smem_bytes(cfg))]
+
+
 PROBLEMS = {"convolution": Convolution, "hotspot": Hotspot, "dedispersion": Dedispersion,
-            "gemm": Gemm}
+            "gemm": Gemm, "gemm_tc": GemmTC}
 
 
 def make_problem(name: str, **kw) -> Problem:

@@ -88,6 +88,8 @@ SIGNATURES = {
                                 C.c_double, C.POINTER(C.c_float)]),
     "tsg_last_launch_times": (C.c_int, [C.c_void_p, C.POINTER(C.c_float), C.c_int]),
     "tsg_event_record": (C.c_int, [C.c_void_p, C.c_int]),
+    "tsg_tma_encode_2d_f32": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_uint64,
+                                        C.c_uint64, C.c_uint32, C.c_uint32, C.c_int]),
     "tsg_event_elapsed": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_float)]),
     "tsg_compare_f32": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_size_t, C.c_double,
                                   C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -370,6 +372,14 @@ class Device:
         t = (C.c_float * n)()
         self.lib.tsg_last_launch_times(self.ctx, t, n)
         return [float(x) for x in t]
+
+    def tma_2d_f32(self, buf: "Buffer", dim0: int, dim1: int, stride1_bytes: int, box0: int, box1: int,
+                   swizzle: int = 128):
+        """CUtensorMap (128 bytes, by-value kernel argument) for a 2-D fp32 tensor."""
+        desc = (C.c_ubyte * 128)()
+        self._check(self.lib.tsg_tma_encode_2d_f32(self.ctx, desc, buf.ptr, dim0, dim1, stride1_bytes,
+                                                   box0, box1, swizzle))
+        return desc
 
     def mark(self, slot: int) -> None:
         """Record stream marker ``slot`` (device-side region timing)."""

@@ -127,3 +127,30 @@ def test_hotspot_large_smem_configs_run(device):
             assert obs.ok, (c, obs)
     finally:
         tgt.close()
+
+
+def test_gemm_tc_tf32_within_k_scaled_tolerance(device):
+    """tcgen05/TMEM/TMA tf32 GEMM vs the fp32 oracle: |dC| <= K * 2^-11 (|a|,|b| <= 1)."""
+    from paper_2407_11488_b200.problems import GemmTC
+
+    prob = GemmTC(m=512, n=512, k=384)
+    want = K.answer(prob)
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        for c in prob.space.enumerate_configs():
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+            st, out = tgt.run_output(c)
+            err = float(np.max(np.abs(out.astype(np.float64) - want)))
+            assert err <= prob.K * 2.0 ** -11, (c, err)
+            assert err > 0  # it really is tf32, not a silent fp32 path
+    finally:
+        tgt.close()
+    big = GemmTC()
+    tgt = CudaTarget(big, device=device)
+    try:
+        obs = tgt.execute((256, 4), PROTO)
+        assert obs.ok, obs
+        assert tgt.extras["256,4"]["verify"]["max_abs_err"] <= big.abs_tol
+    finally:
+        tgt.close()
