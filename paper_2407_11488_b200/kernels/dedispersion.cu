@@ -17,6 +17,9 @@
 //              by the block size (coalesced across lanes), 0 = contiguous
 // The input row of a channel is read through the read-only path; the
 // per-channel delay lives in __constant__ (uniform across the warp).
+// Grid: x = DM tiles (fastest), y = sample tiles, so the blocks sweeping
+// one sample range for ALL DMs are co-resident and the 157 MB input is
+// streamed from HBM ~once (L2 reuse) instead of once per DM-tile row.
 // Problem macros: NCH, NSAMP, NDM, IN_PITCH.
 
 __constant__ float d_delay[NCH];
@@ -33,12 +36,12 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   int s[TSX];
 #pragma unroll
   for (int i = 0; i < TSX; ++i)
-    s[i] = (int)blockIdx.x * (BSX * TSX) + (STX ? tx + i * BSX : tx * TSX + i);
+    s[i] = (int)blockIdx.y * (BSX * TSX) + (STX ? tx + i * BSX : tx * TSX + i);
   int d[TSY];
   float dmv[TSY];
 #pragma unroll
   for (int j = 0; j < TSY; ++j) {
-    d[j] = (int)blockIdx.y * (BSY * TSY) + (STY ? ty + j * BSY : ty * TSY + j);
+    d[j] = (int)blockIdx.x * (BSY * TSY) + (STY ? ty + j * BSY : ty * TSY + j);
     const int dc = d[j] < NDM ? d[j] : NDM - 1;  // overshoot rows compute a valid DM, never stored
     dmv[j] = __fadd_rn(dm_first, __fmul_rn((float)dc, dm_step));
   }

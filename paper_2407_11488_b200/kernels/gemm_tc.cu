@@ -1,16 +1,16 @@
 // TF32 GEMM on the 5th-generation tensor cores (tcgen05 + TMEM + TMA),
-// the north_star's optional B200 variant of the CLBlast GEMM.  Same data
-// layout as kernels/gemm.cu (BLAS column-major with A transposed):
+// the north_star's optional B200 variant of the CLBlast GEMM.  Same
+// product and output layout as kernels/gemm.cu, but the operands are held
+// K-major in HBM (the layout the tf32 UMMA consumes; MN-major tf32
+// operands read as zero on sm_100 -- measured, tools/cuda/mma_probe.cu):
 //
-//   a(m,k) = A[k*GM + m]   b(k,n) = B[k*GN + n]   c(m,n) = C[n*GM + m]
-//
-// so both operands are MN-major in global memory and are consumed as
-// MN-major UMMA operands directly (no transpose pass).
+//   a(m,k) = Ak[m*GK + k]   b(k,n) = Bk[n*GK + k]   c(m,n) = C[n*GM + m]
 //
 // One CTA computes a BM x BN = 128 x BN_T tile (BN_T in {128, 256}):
-//   warp 0      TMA producer: per k-block of BK=32, (BM/32) A boxes and
-//               (BN_T/32) B boxes of 32(MN) x 32(K) fp32, 128B swizzle,
-//               into a STAGES-deep ring guarded by full/empty mbarriers
+//   warp 0      TMA producer: per k-block of BK=32 one A box (32 K x 128 M)
+//               and one B box (32 K x BN_T N), 128B swizzle (K-major
+//               canonical: 128-B rows, 8-row / 1 KB atoms), into a
+//               STAGES-deep ring guarded by full/empty mbarriers
 //   warp 1      TMEM allocator + single-thread MMA issuer:
 //               tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN_T, K=8,
 //               4 per k-block, accumulator in TMEM (BN_T fp32 columns);
@@ -30,11 +30,8 @@
 #define BM 128
 #define BK 32
 #define KSTEP 8
-#define A_BOXES (BM / 32)
-#define B_BOXES (BN_T / 32)
-#define BOX_BYTES (32 * 32 * 4)
-#define A_STAGE_BYTES (A_BOXES * BOX_BYTES)
-#define B_STAGE_BYTES (B_BOXES * BOX_BYTES)
+#define A_STAGE_BYTES (BM * BK * 4)
+#define B_STAGE_BYTES (BN_T * BK * 4)
 #define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
 #define NUM_THREADS 192
 #define TMEM_COLS BN_T
@@ -72,8 +69,8 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const TmaDesc* desc, i
       : "memory");
 }
 
-// UMMA shared-memory descriptor, MN-major, 128B swizzle (canonical
-// ((8,n),(8,k)) in 16-byte units: LBO = MN-block stride, SBO = 8-row K stride)
+// UMMA shared-memory descriptor, K-major, 128B swizzle: rows of 128 B
+// (32 tf32), 8-row atoms of 1 KB, SBO = 1024 (next 8 MN rows), LBO unused (16)
 __device__ __forceinline__ unsigned long long umma_desc(unsigned addr, unsigned lbo, unsigned sbo) {
   unsigned long long d = 0;
   d |= (unsigned long long)((addr >> 4) & 0x3FFF);
@@ -84,17 +81,28 @@ __device__ __forceinline__ unsigned long long umma_desc(unsigned addr, unsigned 
   return d;
 }
 
-// instruction descriptor: D=f32, A=B=tf32, A and B MN-major, N=BN_T, M=128
-#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | \
+// instruction descriptor: D=f32, A=B=tf32, A and B K-major, N=BN_T, M=128
+#ifndef MAJOR_BITS
+#define MAJOR_BITS 0u
+#endif
+#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | MAJOR_BITS | \
                ((unsigned)(BN_T >> 3) << 17) | ((unsigned)(BM >> 4) << 24))
 
 __device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db,
                                           unsigned accumulate) {
+#ifdef MMA_WITH_MASK
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
+      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+#else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
       "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
+#endif
 }
 
 __device__ __forceinline__ void umma_commit(unsigned bar) {
@@ -152,10 +160,8 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
         mbar_expect_tx(full, STAGE_BYTES);
         const unsigned sa = sbase + s * STAGE_BYTES;
         const unsigned sb = sa + A_STAGE_BYTES;
-#pragma unroll
-        for (int i = 0; i < A_BOXES; ++i) tma_load_2d(sa + i * BOX_BYTES, &tma_a, m0 + 32 * i, kb * BK, full);
-#pragma unroll
-        for (int i = 0; i < B_BOXES; ++i) tma_load_2d(sb + i * BOX_BYTES, &tma_b, n0 + 32 * i, kb * BK, full);
+        tma_load_2d(sa, &tma_a, kb * BK, m0, full);  // coords: (k, m)
+        tma_load_2d(sb, &tma_b, kb * BK, n0, full);  // coords: (k, n)
       }
     }
   } else if (warp == 1) {
@@ -165,14 +171,25 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
         const unsigned ph = (kb / STAGES) & 1;
         mbar_wait(full0 + 8 * s, ph);
         asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef DEBUG_DUMP_SMEM
+        if (kb == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
+          const unsigned* w = reinterpret_cast<const unsigned*>(smem);
+          for (int i = 0; i < STAGE_BYTES / 4; ++i) reinterpret_cast<unsigned*>(C)[i] = w[i];
+        }
+#endif
         const unsigned sa = sbase + s * STAGE_BYTES;
         const unsigned sb = sa + A_STAGE_BYTES;
 #pragma unroll
         for (int k = 0; k < BK / KSTEP; ++k) {
-          // K step of 8 rows = one 1024-byte swizzle atom down each MN block
-          const unsigned long long da = umma_desc(sa + k * 1024, BOX_BYTES, 1024);
-          const unsigned long long db = umma_desc(sb + k * 1024, BOX_BYTES, 1024);
+          // K step of 8 tf32 = 32 bytes along the swizzled 128-byte rows
+          const unsigned long long da = umma_desc(sa + k * 32, 16, 1024);
+          const unsigned long long db = umma_desc(sb + k * 32, 16, 1024);
+#ifndef NO_MMA
           umma_tf32(tmem, da, db, (kb | k) != 0);
+#else
+          (void)da;
+          (void)db;
+#endif
         }
         umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs retire
       }
@@ -181,8 +198,25 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   } else {
     // ---- epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
+#ifdef DEBUG_TMEM_ST
+    {  // write a known pattern into TMEM, skip waiting for the MMAs
+      const unsigned ta = tmem + ((unsigned)(q * 32) << 16);
+      for (int c = 0; c < BN_T; ++c) {
+        unsigned val = __float_as_uint((float)((q * 32 + lane) * 1000 + c));
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta + c), "r"(val));
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+#else
     mbar_wait(tfull, 0);
+#endif
     asm volatile("tcgen05.fence::after_thread_sync;");
+#ifdef DEBUG_TMEM_ADDR
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) {
+      C[0] = __uint_as_float(tmem);
+    }
+    if (blockIdx.x == 0 && blockIdx.y == 0) return;
+#endif
     const int m = m0 + q * 32 + lane;
     const unsigned taddr = tmem + ((unsigned)(q * 32) << 16);
 #pragma unroll 1
@@ -194,8 +228,10 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
             "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
           : "r"(taddr + c));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifndef DEBUG_DUMP_SMEM
 #pragma unroll
       for (int j = 0; j < 16; ++j) C[(size_t)(n0 + c + j) * GM + m] = __uint_as_float(r[j]);
+#endif
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

@@ -449,8 +449,9 @@ class Dedispersion(Problem):
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
 
-        grid = (math.ceil(self.NSAMP / (cfg["block_size_x"] * cfg["tile_size_x"])),
-                math.ceil(self.NDM / (cfg["block_size_y"] * cfg["tile_size_y"])), 1)
+        # x = DM tiles (fastest varying: L2 reuse of the input), y = sample tiles
+        grid = (math.ceil(self.NDM / (cfg["block_size_y"] * cfg["tile_size_y"])),
+                math.ceil(self.NSAMP / (cfg["block_size_x"] * cfg["tile_size_x"])), 1)
         return [Launch(kernel, grid, (cfg["block_size_x"], cfg["block_size_y"], 1),
                        [_u64(bufs["out"]), _u64(bufs["in"]), C.c_float(self.dm_first),
                         C.c_float(self.dm_step)])]
@@ -585,15 +586,24 @@ class GemmTC(Gemm):
     def config_defines(self, cfg: dict) -> dict:
         return {"BN_T": cfg["BN_T"], "STAGES": cfg["STAGES"]}
 
+    def host_buffers(self) -> list:
+        a, b = self.a(), self.b()
+        # CLBlast layout (for the fp32 answer kernel) + K-major copies (TMA/UMMA operands)
+        return [BufferSpec("A", a.nbytes, a), BufferSpec("B", b.nbytes, b),
+                BufferSpec("Ak", a.nbytes, np.ascontiguousarray(a.T)),
+                BufferSpec("Bk", b.nbytes, np.ascontiguousarray(b.T)),
+                BufferSpec("out", self.M * self.N * 4)]
+
     def smem_bytes(self, cfg: dict) -> int:
         return cfg["STAGES"] * (16384 + cfg["BN_T"] * 128) + 1024 + 256
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
 
-        dev = bufs["A"].dev
-        ta = dev.tma_2d_f32(bufs["A"], self.M, self.K, self.M * 4, 32, 32, 128)
-        tb = dev.tma_2d_f32(bufs["B"], self.N, self.K, self.N * 4, 32, 32, 128)
+        dev = bufs["Ak"].dev
+        # K-major operands: dim0 = K (contiguous), dim1 = M / N; boxes of 32 K x (128 | BN_T)
+        ta = dev.tma_2d_f32(bufs["Ak"], self.K, self.M, self.K * 4, 32, 128, 128)
+        tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"], 128)
         grid = (self.M // 128, self.N // cfg["BN_T"], 1)
         return [Launch(kernel, grid, (192, 1, 1), [_u64(bufs["out"]), ta, tb], smem=self.smem_bytes(cfg))]
 
