@@ -182,6 +182,7 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dump", default=None, help="write per-configuration results (JSON) here")
     return ap.parse_args(argv)
 
 
@@ -382,6 +383,14 @@ def our_arm(args, dist: Dist):
             cpu = {"value": None, "unit": "configs/s", "cores": None, "kind": "port",
                    "sample": f"unavailable: {e}"}
 
+    if args.dump:
+        rows = []
+        for c, o in results:
+            info = target.extras.get(config_key(c), {})
+            rows.append({"config": list(c), "status": o.status.value, "time_ms": o.time_ms,
+                         "regs": info.get("regs"), "smem": info.get("smem_bytes"),
+                         "launch_ms": info.get("launch_ms")})
+        Path(args.dump).write_text(json.dumps({"workload": args.workload, "rows": rows}))
     all_best = dist.gather_obj(best)
     if dist.rank == 0:
         line = {

@@ -19,7 +19,9 @@
 //   STRM, STRN       1: a thread's vectors are strided by MDIMC*VWM
 //                    (NDIMC*VWN) -- coalesced; 0: contiguous per thread
 //   SA, SB           stage the A / B k-tile in shared memory (else read
-//                    global memory directly inside the k loop)
+//                    global memory directly inside the k loop); staged
+//                    tiles are double-buffered (dynamic smem) with a
+//                    register prefetch of the next k-tile
 // Problem macros: GM, GN, GK.
 
 #ifndef REFERENCE_ONLY
@@ -113,16 +115,29 @@ __device__ __forceinline__ constexpr int vidx_n(int i, int t) {
   return STRN ? i * NDIMC + t : t * (NWI / VWN) + i;
 }
 
+// Software pipeline (our B200 implementation choice, not a tunable): the
+// next k-tile is fetched from HBM into registers while the current one is
+// consumed from shared memory; the staged operands are double-buffered in
+// dynamic shared memory, so each k-tile costs one barrier and its global
+// load latency is hidden behind KWG x MWI x NWI FMAs.
 extern "C" __global__ void __launch_bounds__(MDIMC * NDIMC)
 gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __restrict__ B) {
   const int tid = threadIdx.x;
   const int tx = tid % MDIMC, ty = tid / MDIMC;
   const int m0 = blockIdx.x * MWG, n0 = blockIdx.y * NWG;
+#if SA || SB
+  extern __shared__ float4 gemm_smem4[];
+  float* smem = reinterpret_cast<float*>(gemm_smem4);
+#endif
 #if SA
-  __shared__ __align__(16) float alm[KWG * MWG];
+  float* alm = smem;  // [2][KWG][MWG]
+  const int la0 = tid % MDIMA, la1 = tid / MDIMA;
+  float ra[KWA][MWA / VWM][VWM];
 #endif
 #if SB
-  __shared__ __align__(16) float blm[KWG * NWG];
+  float* blm = smem + (SA ? 2 * KWG * MWG : 0);  // [2][KWG][NWG]
+  const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
+  float rb[KWB][NWB / VWN][VWN];
 #endif
   float acc[NWI][MWI];
 #pragma unroll
@@ -130,48 +145,68 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
 #pragma unroll
     for (int i = 0; i < MWI; ++i) acc[j][i] = 0.f;
 
-  for (int kw = 0; kw < GK; kw += KWG) {
+  auto fetch = [&](int kw) {
 #if SA
-    {
-      const int la0 = tid % MDIMA, la1 = tid / MDIMA;
 #pragma unroll
-      for (int kia = 0; kia < KWA; ++kia)
+    for (int kia = 0; kia < KWA; ++kia)
 #pragma unroll
-        for (int mia = 0; mia < MWA / VWM; ++mia) {
-          const int mv = STRM ? mia * MDIMA + la0 : la0 * (MWA / VWM) + mia;
-          const int kk = kia * KDIMA + la1;
-          float t[VWM];
-          ldv_global<VWM>(t, A + (size_t)(kw + kk) * GM + m0 + mv * VWM);
-          stv<VWM>(alm + kk * MWG + mv * VWM, t);
-        }
-    }
+      for (int mia = 0; mia < MWA / VWM; ++mia) {
+        const int mv = STRM ? mia * MDIMA + la0 : la0 * (MWA / VWM) + mia;
+        ldv_global<VWM>(ra[kia][mia], A + (size_t)(kw + kia * KDIMA + la1) * GM + m0 + mv * VWM);
+      }
 #endif
 #if SB
-    {
-      const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
 #pragma unroll
-      for (int kib = 0; kib < KWB; ++kib)
+    for (int kib = 0; kib < KWB; ++kib)
 #pragma unroll
-        for (int nib = 0; nib < NWB / VWN; ++nib) {
-          const int nv = STRN ? nib * NDIMB + lb0 : lb0 * (NWB / VWN) + nib;
-          const int kk = kib * KDIMB + lb1;
-          float t[VWN];
-          ldv_global<VWN>(t, B + (size_t)(kw + kk) * GN + n0 + nv * VWN);
-          stv<VWN>(blm + kk * NWG + nv * VWN, t);
-        }
-    }
+      for (int nib = 0; nib < NWB / VWN; ++nib) {
+        const int nv = STRN ? nib * NDIMB + lb0 : lb0 * (NWB / VWN) + nib;
+        ldv_global<VWN>(rb[kib][nib], B + (size_t)(kw + kib * KDIMB + lb1) * GN + n0 + nv * VWN);
+      }
 #endif
+  };
+  auto stage = [&](int buf) {
+#if SA
+#pragma unroll
+    for (int kia = 0; kia < KWA; ++kia)
+#pragma unroll
+      for (int mia = 0; mia < MWA / VWM; ++mia) {
+        const int mv = STRM ? mia * MDIMA + la0 : la0 * (MWA / VWM) + mia;
+        stv<VWM>(alm + buf * KWG * MWG + (kia * KDIMA + la1) * MWG + mv * VWM, ra[kia][mia]);
+      }
+#endif
+#if SB
+#pragma unroll
+    for (int kib = 0; kib < KWB; ++kib)
+#pragma unroll
+      for (int nib = 0; nib < NWB / VWN; ++nib) {
+        const int nv = STRN ? nib * NDIMB + lb0 : lb0 * (NWB / VWN) + nib;
+        stv<VWN>(blm + buf * KWG * NWG + (kib * KDIMB + lb1) * NWG + nv * VWN, rb[kib][nib]);
+      }
+#endif
+  };
+  (void)fetch;
+  (void)stage;
+
 #if SA || SB
-    __syncthreads();
+  fetch(0);
+  stage(0);
+  __syncthreads();
 #endif
-#pragma unroll 4
+  int buf = 0;
+  for (int kw = 0; kw < GK; kw += KWG) {
+#if SA || SB
+    const bool more = kw + KWG < GK;
+    if (more) fetch(kw + KWG);  // in flight during the FMAs below
+#endif
+#pragma unroll
     for (int k = 0; k < KWG; ++k) {
       float a[MWI], b[NWI];
 #pragma unroll
       for (int i = 0; i < MWI / VWM; ++i) {
         const int mv = vidx_m(i, tx);
 #if SA
-        ldv<VWM>(a + i * VWM, alm + k * MWG + mv * VWM);
+        ldv<VWM>(a + i * VWM, alm + buf * KWG * MWG + k * MWG + mv * VWM);
 #else
         ldv_global<VWM>(a + i * VWM, A + (size_t)(kw + k) * GM + m0 + mv * VWM);
 #endif
@@ -180,7 +215,7 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
       for (int j = 0; j < NWI / VWN; ++j) {
         const int nv = vidx_n(j, ty);
 #if SB
-        ldv<VWN>(b + j * VWN, blm + k * NWG + nv * VWN);
+        ldv<VWN>(b + j * VWN, blm + buf * KWG * NWG + k * NWG + nv * VWN);
 #else
         ldv_global<VWN>(b + j * VWN, B + (size_t)(kw + k) * GN + n0 + nv * VWN);
 #endif
@@ -191,9 +226,12 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
         for (int i = 0; i < MWI; ++i) acc[j][i] = fmaf(a[i], b[j], acc[j][i]);
     }
 #if SA || SB
+    if (more) stage(buf ^ 1);
     __syncthreads();
+    buf ^= 1;
 #endif
   }
+  (void)buf;
 
 #pragma unroll
   for (int j = 0; j < NWI / VWN; ++j)

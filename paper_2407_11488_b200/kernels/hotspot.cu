@@ -28,7 +28,8 @@
 //     E/W (and the strip ends) are exchanged through a ping-pong pair of
 //     shared buffers: 2 LDS + 1 STS per cell update, 1 barrier per step.
 //   SHARED mode (large tiles): cells live in the shared ping-pong pair;
-//     each column strip is swept top-down with N/C/S in registers:
+//     rows are swept top-down, each row updating the thread's CX columns
+//     (independent -> ILP) with per-column N/C/S windows in registers:
 //     3 LDS + 1 STS per cell update.
 // Blocks whose window lies fully inside the grid take a branch-free
 // path; only edge blocks evaluate the clamping selects.
@@ -75,7 +76,13 @@
 #define HS_GUARD REG_GUARD
 #else
 #define HS_REGISTER_MODE 0
-#define HS_BUF (EH * EW)
+// shared mode: row r lives at ROWB(r); thread-row strips of RY rows are
+// SSS floats apart, SSS = RY*EW + a skew making the 32/BSX strips that
+// share a warp hit disjoint bank groups (same rule as register mode)
+#define SKEW_S ((BSX >= 32) ? 0 : ((BSX - ((RY * EW) % SKEW_M) + SKEW_M) % SKEW_M))
+#define SSS (RY * EW + SKEW_S)
+#define ROWB(r) (((r) / RY) * SSS + ((r) % RY) * EW)
+#define HS_BUF (BSY * SSS)
 #define HS_GUARD (EW + 1)
 #endif
 
@@ -168,10 +175,17 @@ __device__ __forceinline__ void hs_reg_steps(float (&v)[CX][RY], const float* __
 
 #else  // SHARED mode
 
+// Rows outer, the thread's CX columns inner: every row iteration updates
+// CX independent cells (ILP), each column keeping its N/C/S sliding window
+// in registers (3 LDS + 1 STS per update).  Columns outside the active
+// region read a clamped (valid) column and skip the store.
 template <bool EDGE>
 __device__ __forceinline__ float* hs_smem_steps(const float* __restrict__ power, float* A, float* B,
                                                 const float* P, int nsteps, int tx, int r_begin,
                                                 int r_end, int gx0, int gy0, HsCoef k) {
+  int cl[CX];
+#pragma unroll
+  for (int i = 0; i < CX; ++i) cl[i] = min(tx + i * BSX, EW - 1);
   PRAGMA_UNROLL(UNROLL)
   for (int s = 0; s < nsteps; ++s) {
     const int lo = s + 1;
@@ -180,34 +194,46 @@ __device__ __forceinline__ float* hs_smem_steps(const float* __restrict__ power,
       ra = max(ra, -gy0);
       rb = min(rb, GH - gy0);
     }
+    bool cok[CX];
+    float up[CX], mid[CX];
+    const int rl = min(ra, EH - 1);  // padding threads (ra >= rb) must still read in bounds
 #pragma unroll
     for (int i = 0; i < CX; ++i) {
       const int c = tx + i * BSX;
-      const int gx = gx0 + c;
-      if (c < lo || c >= EW - lo || ra >= rb) continue;
-      if (EDGE && (gx < 0 || gx >= GW)) continue;
-      const float* a = A + c;
-      float up = a[(ra - 1) * EW];
-      float mid = a[ra * EW];
-      for (int r = ra; r < rb; ++r) {
-        const float dn = a[(r + 1) * EW];
-        const float t = mid;
-        float n = up, so = dn, w = a[r * EW - 1], e = a[r * EW + 1];
+      cok[i] = (c >= lo) && (c < EW - lo);
+      if (EDGE) cok[i] = cok[i] && (gx0 + c >= 0) && (gx0 + c < GW);
+      up[i] = A[ROWB(rl - 1) + cl[i]];
+      mid[i] = A[ROWB(rl) + cl[i]];
+    }
+#pragma unroll 2
+    for (int r = ra; r < rb; ++r) {
+      const int rowb = ROWB(r);
+      const float* ar = A + rowb;
+      const float* an = A + ROWB(r + 1);
+#pragma unroll
+      for (int i = 0; i < CX; ++i) {
+        const int c = cl[i];
+        const float dn = an[c];
+        const float t = mid[i];
+        float n = up[i], so = dn, w = ar[c - 1], e = ar[c + 1];
         if (EDGE) {
-          const int gy = gy0 + r;
+          const int gy = gy0 + r, gx = gx0 + c;
           n = (gy == 0) ? t : n;
           so = (gy == GH - 1) ? t : so;
           w = (gx == 0) ? t : w;
           e = (gx == GW - 1) ? t : e;
         }
 #if SH_POWER
-        const float p = P[r * EW + c];
+        const float p = P[rowb + c];
 #else
-        const float p = __ldg(power + (size_t)(gy0 + r) * GW + gx);
+        int gxp = gx0 + c;
+        if (EDGE) gxp = min(max(gxp, 0), GW - 1);
+        const float p = __ldg(power + (size_t)(gy0 + r) * GW + gxp);
 #endif
-        B[r * EW + c] = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
-        up = mid;
-        mid = dn;
+        const float u = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
+        if (cok[i]) B[rowb + c] = u;
+        up[i] = t;
+        mid[i] = dn;
       }
     }
     __syncthreads();
@@ -286,9 +312,9 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
       const int c = tx + i * BSX;
       const int gx = gx0 + c;
       if (c < EW && gx >= 0 && gx < GW) {
-        A[r * EW + c] = __ldg(tin + (size_t)gy * GW + gx);
+        A[ROWB(r) + c] = __ldg(tin + (size_t)gy * GW + gx);
 #if SH_POWER
-        P[r * EW + c] = __ldg(power + (size_t)gy * GW + gx);
+        P[ROWB(r) + c] = __ldg(power + (size_t)gy * GW + gx);
 #endif
       }
     }
@@ -305,7 +331,7 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
     for (int i = 0; i < CX; ++i) {
       const int c = tx + i * BSX;
       const int gx = gx0 + c;
-      if (c >= TT && c < TT + OW && gx < GW) out[(size_t)gy * GW + gx] = R[r * EW + c];
+      if (c >= TT && c < TT + OW && gx < GW) out[(size_t)gy * GW + gx] = R[ROWB(r) + c];
     }
   }
 #endif

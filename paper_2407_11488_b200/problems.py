@@ -310,7 +310,8 @@ class Hotspot(Problem):
         reg_bytes = 4 * ((2 + shp) * by * ss + 3 * guard)
         if cx * ry <= cells_max and reg_bytes <= 200 * 1024:
             return "register", by * ss, guard
-        return "shared", eh * ew, ew + 1
+        skew_s = 0 if bx >= 32 else (bx - (ry * ew) % (2 * bx)) % (2 * bx)
+        return "shared", by * (ry * ew + skew_s), ew + 1
 
     def smem_bytes(self, cfg: dict) -> int:
         # (2 + sh_power) window buffers (the space's own smem model,
@@ -526,12 +527,16 @@ class Gemm(Problem):
     def problem_defines(self) -> dict:
         return dict(GM=self.M, GN=self.N, GK=self.K)
 
+    def smem_bytes(self, cfg: dict) -> int:
+        # double-buffered staged k-tiles (kernels/gemm.cu)
+        return 4 * 2 * cfg["KWG"] * (cfg["MWG"] * cfg["SA"] + cfg["NWG"] * cfg["SB"])
+
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
 
         grid = (self.M // cfg["MWG"], self.N // cfg["NWG"], 1)
         return [Launch(kernel, grid, (cfg["MDIMC"] * cfg["NDIMC"], 1, 1),
-                       [_u64(bufs["out"]), _u64(bufs["A"]), _u64(bufs["B"])])]
+                       [_u64(bufs["out"]), _u64(bufs["A"]), _u64(bufs["B"])], smem=self.smem_bytes(cfg))]
 
     def reference_launches(self, kernel, bufs: dict) -> list:
         from .runtime import Launch

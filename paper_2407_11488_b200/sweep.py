@@ -44,7 +44,7 @@ def stratified_sample(space, n: int, seed: int, param: str | None = None, offset
     rng = np.random.default_rng(seed)
     if param is None:
         perm = rng.permutation(len(idx))
-        take = perm[offset: offset + n]
+        take = perm[(offset + np.arange(min(n, len(idx)))) % len(idx)]  # wraps on small spaces
         return space.configs_at(idx[take])
     pi = space.param_names.index(param)
     configs = space.configs_at(idx)
@@ -59,8 +59,8 @@ def stratified_sample(space, n: int, seed: int, param: str | None = None, offset
     for j in range(per):
         for v in keys:
             lst = strata[v]
-            pos = start + j
-            if pos < len(lst) and len(out) < n:
+            pos = (start + j) % len(lst)  # wraps once a stratum is exhausted
+            if len(out) < n:
                 out.append(configs[lst[perms[v][pos]]])
     return out
 
@@ -117,6 +117,15 @@ def roofline(problem, cfg: dict, info: dict, peaks: dict) -> dict:
         flop = problem.FLOP_PER_CELL * problem.W * problem.H * steps[dom]
         byts = 12.0 * problem.W * problem.H
     hbm_peak = peaks["hbm_gbs"] * 1e9
+    if getattr(problem, "space_name", "") == "gemm_tc":
+        # tf32 tensor pipe: dense tf32 = 1/2 dense bf16; denominator = half the
+        # driver-measured cuBLAS bf16 burst (no tf32 figure is measured)
+        tf32 = 0.5 * peaks.get("bf16_tflops", 1639.7)
+        tfs = flop / t / 1e12
+        return {"bound": "tensor", "achieved": round(tfs, 2), "peak": round(tf32, 2), "unit": "TFLOP/s",
+                "frac": round(tfs / tf32, 4), "traffic": None,
+                "peak_source": "0.5 x MEASURED_PEAKS bf16_tflops (tf32 = half-rate bf16)",
+                "alt": {"hbm_gbs": round(byts / t / 1e9, 2)}}
     fp32 = peaks.get("fp32_tflops", 0.0) * 1e12
     t_hbm = byts / hbm_peak
     t_fp = flop / fp32 if fp32 else 0.0

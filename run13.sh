@@ -1,0 +1,6 @@
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "hotspot" > gpurun_out/pytest_hotspot.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --dump gpurun_out/dump_hotspot.json > gpurun_out/bench_hotspot.json 2> gpurun_out/bench_hotspot.err
+timeout 600 python bench.py --workload gemm_tc --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_gemmtc.json 2> gpurun_out/bench_gemmtc.err
