@@ -412,7 +412,10 @@ def our_arm(args, dist: Dist):
             "tuning_impact": impact, "roofline": roof,
             "peaks": {"hbm_gbs": peaks["hbm_gbs"], "hbm_source": peaks["source"],
                       "fp32_tflops": round(peaks["fp32_tflops"], 3),
-                      "fp32_source": "measured in-run (kernels/peak.cu FFMA probe)"},
+                      "ffma_tflops": round(peaks.get("ffma_tflops", 0.0), 3),
+                      "ffma2_tflops": round(peaks.get("ffma2_tflops", 0.0), 3),
+                      "fp32_source": "measured in-run: max of scalar FFMA and packed FFMA2 probes "
+                                     "(kernels/peak.cu)"},
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clocks,
             "setup_s": round(setup_s, 2), "wall_s_timed": round(wall_s, 3),
         }

@@ -125,6 +125,10 @@ int tsg_func_attrs(tsg_kernel* fn, int* num_regs, int* static_smem, int* max_thr
 /* Opt in to >48 KiB dynamic shared memory (hotspot needs up to 64 KiB,
  * ts/spaces/hotspot.spec:25). */
 int tsg_set_max_dynamic_smem(tsg_kernel* fn, int bytes);
+/* Preferred shared-memory carveout of the unified L1/smem (percent of the
+ * maximum, 0..100): kernels that stage tiles in smem ask for 100 so the
+ * occupancy is not capped by a small default carveout. */
+int tsg_set_smem_carveout(tsg_kernel* fn, int percent);
 
 /* Device memory ------------------------------------------------------------ */
 int tsg_alloc(tsg_ctx* ctx, size_t bytes, uint64_t* dptr);

@@ -438,6 +438,13 @@ int tsg_set_max_dynamic_smem(tsg_kernel* k, int bytes) {
   return TSG_OK;
 }
 
+int tsg_set_smem_carveout(tsg_kernel* k, int percent) {
+  if (!k) return fail(TSG_ERR_ARG, "null kernel");
+  CUresult r = cuFuncSetAttribute(k->fn, CU_FUNC_ATTRIBUTE_PREFERRED_SHARED_MEMORY_CARVEOUT, percent);
+  if (r != CUDA_SUCCESS) return fail(TSG_ERR_INVALID, "carveout: " + cu_msg(r));
+  return TSG_OK;
+}
+
 int tsg_alloc(tsg_ctx* c, size_t bytes, uint64_t* dptr) {
   int s = make_current(c);
   if (s) return s;

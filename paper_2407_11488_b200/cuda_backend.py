@@ -211,6 +211,8 @@ class CudaTarget:
             if smem > 48 * 1024:
                 if kern.set_max_dynamic_smem(smem) != rt.OK:
                     return Observation(Status.INVALID, detail=rt.last_error())
+            if smem > 0:
+                kern.set_smem_carveout(100)  # occupancy limited by smem use, not a default carveout
             info.update(kern.attrs())
             info["smem_bytes"] = smem
             launches = self.problem.launches(cfg, kern, self.bufs)
@@ -263,6 +265,8 @@ class CudaTarget:
             smem = self.problem.smem_bytes(cfg)
             if smem > 48 * 1024 and kern.set_max_dynamic_smem(smem) != rt.OK:
                 return Status.INVALID, rt.last_error()
+            if smem > 0:
+                kern.set_smem_carveout(100)
             self.dev._check(self.dev.lib.tsg_memset32(self.dev.ctx, self.out.ptr, 0x7FC00000,
                                                       self.n_out))
             rc, err = self.dev.run(self.problem.launches(cfg, kern, self.bufs))

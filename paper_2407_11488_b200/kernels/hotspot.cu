@@ -23,10 +23,12 @@
 // Thread (tx, ty) owns window columns tx + i*BSX (coalesced, bank-
 // conflict free) and a CONTIGUOUS run of RY rows.  Two schedules,
 // chosen at compile time from the register budget:
-//   REGISTER mode (CX*RY small): the thread's cells live in registers
-//     across all steps; N/S neighbours come from its own registers, only
-//     E/W (and the strip ends) are exchanged through a ping-pong pair of
-//     shared buffers: 2 LDS + 1 STS per cell update, 1 barrier per step.
+//   REGISTER mode (small per-thread footprint): the thread owns PAIRS of
+//     adjacent columns held in float2 registers across all steps; N/S come
+//     from its own registers, only E/W (and the strip ends) are exchanged
+//     through a ping-pong pair of shared buffers; arithmetic is packed
+//     FFMA2/FADD2 (sm_100): per 2 cells 2 LDS + 1 STS.64 + 9 packed ops,
+//     1 barrier per step; sh_power keeps the power tile in registers.
 //   SHARED mode (large tiles): cells live in the shared ping-pong pair;
 //     rows are swept top-down, each row updating the thread's CX columns
 //     (independent -> ILP) with per-column N/C/S windows in registers:
@@ -57,20 +59,25 @@
 
 // register budget per thread under __launch_bounds__(NTHREADS)
 #define REG_BUDGET ((65536 / NTHREADS) > 255 ? 255 : (65536 / NTHREADS))
-#define REG_CELLS_MAX (((REG_BUDGET - 40) / 2) < 32 ? ((REG_BUDGET - 40) / 2) : 32)
-// padded window of register mode: row pitch SP, RT rows; each thread-row
-// strip of RY rows starts SS floats after the previous one, SS = RY*SP +
-// a skew chosen so that the 32/BSX thread rows sharing a warp land on
-// disjoint bank groups (SS = BSX * odd (mod 32)) -- no bank conflicts.
-#define SP (CX * BSX)
+// register mode works on PAIRS of adjacent columns (float2, packed FFMA2):
+// CXP pairs per thread, 2 (value) + 2 (new value) + 2*SH_POWER (power)
+// registers per pair
+#define CXP ((EW + 2 * BSX - 1) / (2 * BSX))
+#define REG_PAIRS_MAX (((REG_BUDGET - 40) / (4 + 2 * SH_POWER)) < 16 ? ((REG_BUDGET - 40) / (4 + 2 * SH_POWER)) : 16)
+// padded window: row pitch SP floats, thread-row strips of RY rows SS
+// floats apart; SS = RY*SP + a skew so that the 32/BSX thread rows sharing
+// a warp hit disjoint bank groups with 8-byte accesses (SS = 2*BSX*odd
+// (mod 4*BSX) when 2*BSX < 32) -- no bank conflicts
+#define SP (2 * CXP * BSX)
 #define RT (RY * BSY)
-#define SKEW_M (2 * BSX)
-#define SKEW ((BSX >= 32) ? 0 : ((BSX - ((RY * SP) % SKEW_M) + SKEW_M) % SKEW_M))
+#define PSKEW_M (4 * BSX)
+#define SKEW ((2 * BSX >= 32) ? 0 : ((2 * BSX - ((RY * SP) % PSKEW_M) + PSKEW_M) % PSKEW_M))
 #define SS (RY * SP + SKEW)
-#define REG_GUARD (SP + 33)
-#define REG_SMEM_BYTES (4 * ((2 + SH_POWER) * BSY * SS + 3 * REG_GUARD))
+#define REG_GUARD (SP + 34)
+#define REG_SMEM_BYTES (4 * (2 * BSY * SS + 3 * REG_GUARD))
 // (mirrored on the host by problems.Hotspot.kernel_mode / smem_bytes)
-#if !defined(HS_FORCE_SHARED) && (CX * RY <= REG_CELLS_MAX) && (REG_SMEM_BYTES <= 200 * 1024)
+#define SKEW_M (2 * BSX)
+#if !defined(HS_FORCE_SHARED) && (CXP * RY <= REG_PAIRS_MAX) && (REG_SMEM_BYTES <= 200 * 1024)
 #define HS_REGISTER_MODE 1
 #define HS_BUF (BSY * SS)
 #define HS_GUARD REG_GUARD
@@ -92,78 +99,111 @@ struct HsCoef {
 
 #if HS_REGISTER_MODE
 
-// Register mode works on a PADDED window: row pitch SP = CX*BSX and RT =
-// RY*BSY rows, so every thread cell (i, j) has its own smem slot at the
-// affine index tb + j*SP + i*BSX (compile-time offsets from one per-thread
-// base).  Cells are computed branch-free; activity (the shrinking valid
-// region, domain edges) is one select per cell from per-row / per-column
-// predicates evaluated once per step, and rows with no active cell in the
-// warp are skipped with a warp-uniform test.  Guard bands of SP+1 floats
-// before/after each buffer keep the +-1 / +-SP reads of border cells in
-// bounds; those values only ever feed inactive (discarded) cells.
+// Register mode: thread (tx,ty) owns column PAIRS (2p, 2p+1), p = tx + i*BSX,
+// over a contiguous strip of RY rows, values held in float2 registers across
+// all steps.  A step per pair: 2 scalar LDS (W of the left column, E of the
+// right one; N/S come from registers except at strip ends), the 9
+// arithmetic ops of HS_STEP as PACKED fp32x2 instructions (FFMA2/FADD2,
+// sm_100; per component identical to the scalar fmaf/fadd -> bit-exact),
+// and one 8-byte STS.  Rows with no active cell in the warp are skipped
+// (warp-uniform vote).  Smem is a padded, skewed layout (no bank
+// conflicts) with guard bands absorbing the border over-reach.
+__device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
+
+struct HsCoef2 {  // coefficient pairs, built once per launch
+  float2 sdc, rx1, ry1, rz1, amb;
+};
+
+__device__ __forceinline__ float2 hs_step2(float2 t, float2 n, float2 s, float2 e, float2 w, float2 p,
+                                           const HsCoef2& k) {
+  const float2 m2 = f2(-2.0f, -2.0f);
+  const float2 m1 = f2(-1.0f, -1.0f);
+  const float2 ns = __ffma2_rn(m2, t, __fadd2_rn(n, s));
+  const float2 ew = __ffma2_rn(m2, t, __fadd2_rn(e, w));
+  float2 d = __ffma2_rn(ns, k.ry1, p);
+  d = __ffma2_rn(ew, k.rx1, d);
+  const float2 z = __ffma2_rn(t, m1, k.amb);  // amb - t, one rounding
+  d = __ffma2_rn(z, k.rz1, d);
+  return __ffma2_rn(k.sdc, d, t);
+}
+
 template <bool EDGE>
-__device__ __forceinline__ void hs_reg_steps(float (&v)[CX][RY], const float* __restrict__ power,
-                                             float* A, float* B, const float* P, int nsteps,
-                                             int tx, int r0, int gx0, int gy0, HsCoef k) {
-  const int tb = (r0 / RY) * SS + tx;  // strip of thread row r0/RY
+__device__ __forceinline__ void hs_reg_steps(float2 (&v)[CXP][RY], const float2 (&pw)[CXP][RY],
+                                             const float* __restrict__ power, float* A, float* B,
+                                             int nsteps, int tx, int ty, int gx0, int gy0, HsCoef kk) {
+  const HsCoef2 k{f2(kk.sdc, kk.sdc), f2(kk.rx1, kk.rx1), f2(kk.ry1, kk.ry1), f2(kk.rz1, kk.rz1),
+                  f2(kk.amb, kk.amb)};
+  const int tb = ty * SS + 2 * tx;
+  const int r0 = ty * RY;
   PRAGMA_UNROLL(UNROLL)
   for (int s = 0; s < nsteps; ++s) {
     const int lo = s + 1;
-    float nv[CX][RY];
-    bool col_ok[CX];
+    float2 nv[CXP][RY];
+    bool ok0[CXP], ok1[CXP];
 #pragma unroll
-    for (int i = 0; i < CX; ++i) {
-      const int c = tx + i * BSX;
-      col_ok[i] = (c >= lo) && (c < EW - lo);
-      if (EDGE) col_ok[i] = col_ok[i] && (gx0 + c >= 0) && (gx0 + c < GW);
+    for (int i = 0; i < CXP; ++i) {
+      const int c0 = 2 * (tx + i * BSX);
+      ok0[i] = (c0 >= lo) && (c0 < EW - lo);
+      ok1[i] = (c0 + 1 >= lo) && (c0 + 1 < EW - lo);
+      if (EDGE) {
+        ok0[i] = ok0[i] && (gx0 + c0 >= 0) && (gx0 + c0 < GW);
+        ok1[i] = ok1[i] && (gx0 + c0 + 1 >= 0) && (gx0 + c0 + 1 < GW);
+      }
     }
 #pragma unroll
     for (int j = 0; j < RY; ++j) {
       const int r = r0 + j;
       bool row_ok = (r >= lo) && (r < EH - lo);
       if (EDGE) row_ok = row_ok && (gy0 + r >= 0) && (gy0 + r < GH);
-      float* bj = B + tb + j * SP;
       if (__any_sync(0xffffffffu, row_ok)) {
         const float* aj = A + tb + j * SP;
+        float* bj = B + tb + j * SP;
 #pragma unroll
-        for (int i = 0; i < CX; ++i) {
-          const float t = v[i][j];
-          // strip ends: the neighbour row lives in the adjacent strip
-          float n = (j > 0) ? v[i][j - 1] : aj[i * BSX + (RY - 1) * SP - SS];
-          float so = (j < RY - 1) ? v[i][j + 1] : aj[i * BSX + SS - (RY - 1) * SP];
-          float w = aj[i * BSX - 1];
-          float e = aj[i * BSX + 1];
+        for (int i = 0; i < CXP; ++i) {
+          const float2 t = v[i][j];
+          float2 n = (j > 0) ? v[i][j - 1]
+                             : *reinterpret_cast<const float2*>(aj + 2 * i * BSX + (RY - 1) * SP - SS);
+          float2 so = (j < RY - 1) ? v[i][j + 1]
+                                   : *reinterpret_cast<const float2*>(aj + 2 * i * BSX + SS - (RY - 1) * SP);
+          float2 w = f2(aj[2 * i * BSX - 1], t.x);
+          float2 e = f2(t.y, aj[2 * i * BSX + 2]);
+          float2 p;
           if (EDGE) {
-            const int gx = gx0 + tx + i * BSX, gy = gy0 + r;
+            const int gx = gx0 + 2 * (tx + i * BSX), gy = gy0 + r;
             n = (gy == 0) ? t : n;
             so = (gy == GH - 1) ? t : so;
-            w = (gx == 0) ? t : w;
-            e = (gx == GW - 1) ? t : e;
+            w.x = (gx == 0) ? t.x : w.x;
+            w.y = (gx + 1 == 0) ? t.y : w.y;
+            e.x = (gx == GW - 1) ? t.x : e.x;
+            e.y = (gx + 1 == GW - 1) ? t.y : e.y;
           }
 #if SH_POWER
-          const float p = P[tb + j * SP + i * BSX];
+          p = pw[i][j];
 #else
-          int gyp = gy0 + r, gxp = gx0 + tx + i * BSX;
-          if (EDGE) {
-            gyp = min(max(gyp, 0), GH - 1);
-            gxp = min(max(gxp, 0), GW - 1);
+          {
+            int gyp = gy0 + r, gxp = gx0 + 2 * (tx + i * BSX);
+            int gxq = gxp + 1;
+            if (EDGE) {
+              gyp = min(max(gyp, 0), GH - 1);
+              gxp = min(max(gxp, 0), GW - 1);
+              gxq = min(max(gxq, 0), GW - 1);
+            }
+            p = f2(__ldg(power + (size_t)gyp * GW + gxp), __ldg(power + (size_t)gyp * GW + gxq));
           }
-          const float p = __ldg(power + (size_t)gyp * GW + gxp);
 #endif
-          const float u = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
-          nv[i][j] = (row_ok && col_ok[i]) ? u : t;
-          bj[i * BSX] = nv[i][j];
+          const float2 u = hs_step2(t, n, so, e, w, p, k);
+          nv[i][j] = f2((row_ok && ok0[i]) ? u.x : t.x, (row_ok && ok1[i]) ? u.y : t.y);
+          *reinterpret_cast<float2*>(bj + 2 * i * BSX) = nv[i][j];
         }
       } else {
+        // no active cell of this row in the warp: unchanged, and never read
+        // by an active cell of a later step (the active region only shrinks)
 #pragma unroll
-        for (int i = 0; i < CX; ++i) {
-          nv[i][j] = v[i][j];
-          bj[i * BSX] = v[i][j];
-        }
+        for (int i = 0; i < CXP; ++i) nv[i][j] = v[i][j];
       }
     }
 #pragma unroll
-    for (int i = 0; i < CX; ++i)
+    for (int i = 0; i < CXP; ++i)
 #pragma unroll
       for (int j = 0; j < RY; ++j) v[i][j] = nv[i][j];
     __syncthreads();
@@ -255,7 +295,8 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   // absorb register mode's one-row/one-column overreach at the borders
   float* A = smem + HS_GUARD;
   float* B = A + HS_BUF + HS_GUARD;
-  float* P = B + HS_BUF + HS_GUARD;  // used only when SH_POWER
+  float* P = B + HS_BUF + HS_GUARD;  // shared mode with SH_POWER only
+  (void)P;
   const HsCoef k{sdc, rx1, ry1, rz1, amb};
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int gx0 = (int)blockIdx.x * OW - TT;
@@ -267,40 +308,45 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   // interior: the whole PADDED window maps inside the grid (padding cells
   // then read valid global addresses and need no clamping)
   const bool interior = gx0 >= 0 && gy0 >= 0 && gx0 + SP <= GW && gy0 + RT <= GH;
-  float v[CX][RY];
-  const int tb = ty * SS + tx;
+  float2 v[CXP][RY];
+  float2 pw[CXP][RY];
+  const int tb = ty * SS + 2 * tx;
 #pragma unroll
-  for (int i = 0; i < CX; ++i) {
-    const int c = tx + i * BSX;
-    const int gx = gx0 + c;
+  for (int i = 0; i < CXP; ++i) {
+    const int gx = gx0 + 2 * (tx + i * BSX);
 #pragma unroll
     for (int j = 0; j < RY; ++j) {
       const int gy = gy0 + r_begin + j;
-      v[i][j] = 0.f;
-      if (interior || (gx >= 0 && gx < GW && gy >= 0 && gy < GH)) {
-        v[i][j] = __ldg(tin + (size_t)gy * GW + gx);
+      const bool in_y = interior || (gy >= 0 && gy < GH);
+      const bool in0 = in_y && (interior || (gx >= 0 && gx < GW));
+      const bool in1 = in_y && (interior || (gx + 1 >= 0 && gx + 1 < GW));
+      const size_t o = (size_t)gy * GW + gx;
+      v[i][j] = f2(in0 ? __ldg(tin + o) : 0.f, in1 ? __ldg(tin + o + 1) : 0.f);
 #if SH_POWER
-        P[tb + j * SP + i * BSX] = __ldg(power + (size_t)gy * GW + gx);
+      pw[i][j] = f2(in0 ? __ldg(power + o) : 0.f, in1 ? __ldg(power + o + 1) : 0.f);
+#else
+      pw[i][j] = f2(0.f, 0.f);
 #endif
-      }
-      A[tb + j * SP + i * BSX] = v[i][j];
+      *reinterpret_cast<float2*>(A + tb + j * SP + 2 * i * BSX) = v[i][j];
     }
   }
   __syncthreads();
   if (interior)
-    hs_reg_steps<false>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
+    hs_reg_steps<false>(v, pw, power, A, B, nsteps, tx, ty, gx0, gy0, k);
   else
-    hs_reg_steps<true>(v, power, A, B, P, nsteps, tx, r_begin, gx0, gy0, k);
+    hs_reg_steps<true>(v, pw, power, A, B, nsteps, tx, ty, gx0, gy0, k);
 #pragma unroll
-  for (int i = 0; i < CX; ++i) {
-    const int c = tx + i * BSX;
+  for (int i = 0; i < CXP; ++i) {
+    const int c = 2 * (tx + i * BSX);
     const int gx = gx0 + c;
 #pragma unroll
     for (int j = 0; j < RY; ++j) {
       const int r = r_begin + j;
       const int gy = gy0 + r;
-      if (c >= TT && c < TT + OW && r >= TT && r < TT + OH && gx < GW && gy < GH)
-        out[(size_t)gy * GW + gx] = v[i][j];
+      if (r >= TT && r < TT + OH && gy < GH) {
+        if (c >= TT && c < TT + OW && gx < GW) out[(size_t)gy * GW + gx] = v[i][j].x;
+        if (c + 1 >= TT && c + 1 < TT + OW && gx + 1 < GW) out[(size_t)gy * GW + gx + 1] = v[i][j].y;
+      }
     }
   }
 #else

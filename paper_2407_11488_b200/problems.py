@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 from pathlib import Path
 
@@ -90,7 +91,11 @@ class Problem:
         return {k.upper(): int(v) for k, v in cfg.items()}
 
     def options(self, cfg: dict | None) -> list:
-        opts = ["--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"] + list(self.extra_options)
+        # -lineinfo costs ~25% NVRTC time per configuration: only for profiling
+        # builds (TSG_LINEINFO=1, set by tools/run_config.py for ncu)
+        opts = ["--gpu-architecture=sm_100a", "-std=c++17"] + list(self.extra_options)
+        if os.environ.get("TSG_LINEINFO"):
+            opts.append("-lineinfo")
         d = dict(self.problem_defines())
         if cfg is not None:
             d.update(self.config_defines(cfg))
@@ -295,30 +300,31 @@ class Hotspot(Problem):
 
     @staticmethod
     def kernel_mode(cfg: dict) -> tuple:
-        """(mode, floats per buffer, guard floats) -- mirrors kernels/hotspot.cu macros."""
+        """(mode, floats per buffer, guard floats, buffers) -- mirrors kernels/hotspot.cu macros."""
         bx, by = cfg["block_size_x"], cfg["block_size_y"]
         t, shp = cfg["temporal_tiling_factor"], cfg["sh_power"]
         ew = bx * cfg["tile_size_x"] + 2 * t
         eh = by * cfg["tile_size_y"] + 2 * t
-        cx, ry = -(-ew // bx), -(-eh // by)
+        ry = -(-eh // by)
         budget = min(255, 65536 // (bx * by))
-        cells_max = min(32, (budget - 40) // 2)
-        sp = cx * bx
-        skew = 0 if bx >= 32 else (bx - (ry * sp) % (2 * bx)) % (2 * bx)
+        cxp = -(-ew // (2 * bx))
+        pairs_max = min(16, (budget - 40) // (4 + 2 * shp))
+        sp = 2 * cxp * bx
+        skew = 0 if 2 * bx >= 32 else (2 * bx - (ry * sp) % (4 * bx)) % (4 * bx)
         ss = ry * sp + skew
-        guard = sp + 33
-        reg_bytes = 4 * ((2 + shp) * by * ss + 3 * guard)
-        if cx * ry <= cells_max and reg_bytes <= 200 * 1024:
-            return "register", by * ss, guard
+        guard = sp + 34
+        reg_bytes = 4 * (2 * by * ss + 3 * guard)
+        if cxp * ry <= pairs_max and reg_bytes <= 200 * 1024:
+            return "register", by * ss, guard, 2  # power lives in registers
         skew_s = 0 if bx >= 32 else (bx - (ry * ew) % (2 * bx)) % (2 * bx)
-        return "shared", by * (ry * ew + skew_s), ew + 1
+        return "shared", by * (ry * ew + skew_s), ew + 1, 2 + shp
 
     def smem_bytes(self, cfg: dict) -> int:
-        # (2 + sh_power) window buffers (the space's own smem model,
-        # ts/spaces/hotspot.spec:25; register mode pads rows/columns to the
-        # thread grid) + three pitch+1 guard bands
-        _, buf, guard = self.kernel_mode(cfg)
-        return 4 * ((2 + cfg["sh_power"]) * buf + 3 * guard)
+        # window buffers (the space's own smem model is (2 + sh_power) x
+        # window, ts/spaces/hotspot.spec:25; we pad/skew them and add three
+        # guard bands -- register mode keeps power in registers)
+        _, buf, guard, nbuf = self.kernel_mode(cfg)
+        return 4 * (nbuf * buf + 3 * guard)
 
     def step_plan(self, t: int) -> list:
         n = math.ceil(self.iterations / t)

@@ -75,6 +75,7 @@ SIGNATURES = {
     "tsg_set_constant": (C.c_int, [C.c_void_p, C.c_char_p, C.c_void_p, C.c_size_t]),
     "tsg_func_attrs": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 4),
     "tsg_set_max_dynamic_smem": (C.c_int, [C.c_void_p, C.c_int]),
+    "tsg_set_smem_carveout": (C.c_int, [C.c_void_p, C.c_int]),
     "tsg_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "tsg_free": (C.c_int, [C.c_void_p, C.c_uint64]),
     "tsg_h2d": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_size_t]),
@@ -244,6 +245,9 @@ class Kernel:
 
     def set_max_dynamic_smem(self, nbytes: int) -> int:
         return self.module.dev.lib.tsg_set_max_dynamic_smem(self.handle, int(nbytes))
+
+    def set_smem_carveout(self, percent: int) -> int:
+        return self.module.dev.lib.tsg_set_smem_carveout(self.handle, int(percent))
 
 
 class Launch:

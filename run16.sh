@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 300 python __graft_entry__.py > gpurun_out/smoke.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "hotspot" > gpurun_out/pytest_hotspot.log 2>&1
+timeout 600 python bench.py --no-cpu-baseline --no-e2e --dump gpurun_out/dump_hotspot.json > gpurun_out/bench_hotspot.json 2> gpurun_out/bench_hotspot.err
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:hotspot_kernel -s 4 -c 1 -o gpurun_out/prof_hotspot_best2 -f python tools/run_config.py hotspot 32,16,3,2,6,6,1 --runs 2 > gpurun_out/ncu_hotspot_best2.log 2>&1

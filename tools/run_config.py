@@ -3,10 +3,12 @@
     python tools/run_config.py hotspot 64,4,2,4,10,2,1 [--runs 3]
 """
 import argparse
+import os
 import sys
 from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+os.environ.setdefault("TSG_LINEINFO", "1")  # source-level ncu pages
 
 from paper_2407_11488_b200.cuda_backend import CudaTarget  # noqa: E402
 from paper_2407_11488_b200.measure import MeasurementProtocol  # noqa: E402
