@@ -45,6 +45,354 @@
 
 #ifndef REFERENCE_ONLY
 
+struct HsCoef {
+  float sdc, rx1, ry1, rz1, amb;
+};
+
+#if defined(HS_STREAM) && HS_STREAM
+// ============================================================================
+// STREAM mode (the host selects it when the register/smem budget allows).
+//
+// The unit of work is a WARP, not a block: warp w streams down a strip of
+// SW = 32*TSX window columns (lane L owns the TSX contiguous columns
+// L*TSX..L*TSX+TSX-1) and produces the UW useful columns of SEGH = 32*TSY
+// output rows.  The nsteps <= TT time levels are pipelined along the stream
+// (time skewing): when input row i arrives, level k is advanced at row
+// i-k for k = 1..nsteps, so every level keeps only a 3-row ring in
+// registers (R[k][3][.]) and level nsteps leaves the pipeline one row per
+// iteration.  Neighbours: N/S from the register ring, E/W of the lane's
+// edge columns by warp shuffles (2 SHFL per lane per level): no block
+// barrier and no shared-memory exchange.  Halo cost: the strip recomputes
+// TA+TT columns (UW = floor4(SW - TA - TT) useful) and each segment streams
+// SEGH + 2*nsteps rows.
+//
+// Memory: every lane stages ITS OWN columns, so no lane ever waits for
+// another: input rows arrive by cp.async (LDGSTS, 16/8/4-byte chunks,
+// zero-fill outside the grid) into an NR-row per-warp shared ring, NR-1
+// rows in flight, completion by per-thread cp.async groups (no mbarrier,
+// no __syncwarp).  SH_POWER=1 stages power rows the same way in a PR-row
+// ring (each power row serves TT levels); SH_POWER=0 re-reads power
+// through L1 per level.  Output rows leave by direct vector stores (window
+// origin and UW are multiples of 4 columns, so every 16-byte chunk is
+// aligned and either fully useful or not).  Chunks are laid out
+// chunk-major in shared memory (bank-conflict-free vector LDS).
+// Arithmetic is packed FFMA2/FADD2 on column pairs, per component
+// identical to HS_STEP (bit-exact).
+//
+// loop_unroll_factor_t: the level loop is always fully unrolled (its
+// registers are indexed by level); the row stream is unrolled by 3 (ring
+// phases).  Mapping of the tunables: block = (BSX, BSY) threads = WPB warps
+// taking consecutive warp tiles (strip-fastest), TSX = columns per lane,
+// TSY = output rows per lane / 32, TT = levels per launch.
+// ============================================================================
+
+#define SW (32 * TSX)
+#define TA (((TT) + 3) & ~3)
+#define UW (((SW - TA - TT) / 4) * 4)
+#define SEGH (32 * TSY)
+#define NSTRIPS ((GW + UW - 1) / UW)
+#define NSEGS ((GH + SEGH - 1) / SEGH)
+#define NTHREADS (BSX * BSY)
+#define WPB (NTHREADS / 32)
+#define NR 4
+// power ring: a power of two >= TT + NR rows (slot = row & (PR - 1))
+#define PR (SH_POWER ? ((TT + NR) <= 8 ? 8 : 16) : 0)
+#define WARP_FLOATS (SW * (NR + PR))
+// staging chunk (floats) and chunks per lane
+#define CW ((TSX % 4) == 0 ? 4 : ((TSX % 2) == 0 ? 2 : 1))
+#define NCH (TSX / CW)
+#define NP2 ((TSX + 1) / 2)
+#define COL(v, j) ((j) % 2 == 0 ? (v)[(j) / 2].x : (v)[(j) / 2].y)
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+
+// one staging chunk, zero-filled when `bytes` == 0 (outside the grid)
+__device__ __forceinline__ void cp_chunk(float* dst, const float* src, unsigned bytes) {
+#if CW == 4
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+               : "memory");
+#elif CW == 2
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+               : "memory");
+#else
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes)
+               : "memory");
+#endif
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+struct HsK2 {
+  float2 sdc, rx1, ry1, rz1, amb;
+};
+
+struct HsStream {
+  const float* tin;
+  const float* power;
+  float* out;
+  float* tring;   // NR rows, chunk-major
+  float* pring;   // PR rows (SH_POWER)
+  int lane, gx0, ia, ib, y0, y1, nsteps;
+  int cbytes[NCH];   // staging bytes per chunk (0 outside the grid)
+  int csrc[NCH];     // global column of each chunk (clamped into the grid)
+  unsigned omask;    // chunks that are useful output columns
+  unsigned lmask, rmask;  // owned cells at gx == 0 / gx == GW-1
+};
+
+// chunk c of this lane inside a shared row (chunk-major: lanes contiguous)
+__device__ __forceinline__ float* chunk_ptr(float* row, int c, int lane) { return row + (c * 32 + lane) * CW; }
+
+__device__ __forceinline__ void lds_pairs(float2 (&v)[NP2], const float* row, int lane) {
+  float t[TSX];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const float* p = row + (c * 32 + lane) * CW;
+#if CW == 4
+    const float4 q = *reinterpret_cast<const float4*>(p);
+    t[4 * c] = q.x; t[4 * c + 1] = q.y; t[4 * c + 2] = q.z; t[4 * c + 3] = q.w;
+#elif CW == 2
+    const float2 q = *reinterpret_cast<const float2*>(p);
+    t[2 * c] = q.x; t[2 * c + 1] = q.y;
+#else
+    t[c] = *p;
+#endif
+  }
+#pragma unroll
+  for (int q = 0; q < NP2; ++q) v[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
+}
+
+// stage input (and power) row `row` into the rings; always commits a group
+// so that group counting stays uniform
+__device__ __forceinline__ void hs_stage_row(const HsStream& S, int row) {
+  if (row <= S.ib && row < GH) {
+    const size_t rb = (size_t)row * GW;
+    float* tr = S.tring + ((row - S.ia) & (NR - 1)) * SW;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) cp_chunk(chunk_ptr(tr, c, S.lane), S.tin + rb + S.csrc[c], S.cbytes[c]);
+#if SH_POWER
+    float* pr = S.pring + ((row - S.ia) & (PR - 1)) * SW;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) cp_chunk(chunk_ptr(pr, c, S.lane), S.power + rb + S.csrc[c], S.cbytes[c]);
+#endif
+  }
+  cp_commit();
+}
+
+// Fetch the operands of iteration i: its input row (landed by cp.async)
+// and the E/W neighbours of every level's centre row (level k-1 row i-k,
+// all computed by earlier iterations) -- all shuffled in ONE convergence
+// block, so the level chain that follows is straight-line code.  (Issuing
+// this at the end of iteration i-1 instead was measured slower.)
+template <int PH>
+__device__ __forceinline__ void hs_fetch(const HsStream& S, const float2 (&R)[TT][3][NP2], int i,
+                                         float2 (&cur)[NP2], float (&wls)[TT], float (&ers)[TT]) {
+  hs_stage_row(S, i + NR - 1);  // keep NR-1 rows in flight
+  cp_wait<NR - 1>();            // this lane's chunks of row i have landed
+  lds_pairs(cur, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    const int sC = ((PH - k) % 3 + 3) % 3;
+    wls[k - 1] = __shfl_up_sync(0xffffffffu, COL(R[k - 1][sC], TSX - 1), 1);
+    ers[k - 1] = __shfl_down_sync(0xffffffffu, R[k - 1][sC][0].x, 1);
+  }
+}
+
+// One stream iteration: input row i (in cur) advances level k at row i-k.
+// PH = (i - ia) mod 3 fixes every register-ring slot at compile time.
+template <int PH, bool EDGE, bool FULL>
+__device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT][3][NP2], int i,
+                                               float2 (&cur)[NP2], float (&wls)[TT], float (&ers)[TT],
+                                               const HsCoef& kk, const HsK2& k2) {
+  const int lane = S.lane;
+  hs_fetch<PH>(S, R, i, cur, wls, ers);
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    if (!FULL && k > S.nsteps) break;  // FULL: nsteps == TT (static: no exit phis)
+    const int r = i - k;  // row produced at level k
+    // ring slots of level k-1 rows r-1, r, r+1 (static after unrolling)
+    const int sN = ((PH - k - 1) % 3 + 3) % 3;
+    const int sC = ((PH - k) % 3 + 3) % 3;
+    const int sS = ((PH - k + 1) % 3 + 3) % 3;
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) R[k - 1][sS][q] = cur[q];  // level k-1 row r+1
+    const float2* RN = R[k - 1][sN];
+    const float2* RC = R[k - 1][sC];
+    const float wl = wls[k - 1], er = ers[k - 1];
+    float2 pw[NP2];
+#if SH_POWER
+    lds_pairs(pw, S.pring + ((r - S.ia) & (PR - 1)) * SW, lane);
+#else
+    {
+      const float* prow = S.power + (size_t)min(max(r, 0), GH - 1) * GW;
+      float t[TSX];
+#pragma unroll
+      for (int c = 0; c < NCH; ++c) {
+        const float* p = prow + S.csrc[c];
+#if CW == 4
+        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+        t[4 * c] = q.x; t[4 * c + 1] = q.y; t[4 * c + 2] = q.z; t[4 * c + 3] = q.w;
+#elif CW == 2
+        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
+        t[2 * c] = q.x; t[2 * c + 1] = q.y;
+#else
+        t[c] = __ldg(p);
+#endif
+      }
+#pragma unroll
+      for (int q = 0; q < NP2; ++q) pw[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
+    }
+#endif
+    const bool top = EDGE && (r == 0), bot = EDGE && (r == GH - 1);
+    float2 nv[NP2];
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) {
+      const int j = 2 * q;
+      const float2 t = RC[q];
+      float2 n = RN[q], s = cur[q];
+      // west / east neighbours of columns j and j+1 straddle the register
+      // pairs: form them as scalars and add them with two scalar FADDs
+      // (the FMA pipe cost of one FADD2) instead of moving registers
+      float w0 = (j == 0) ? wl : COL(RC, j - 1);
+      float e0 = (j + 1 < TSX) ? t.y : er;
+      float w1 = t.x;
+      float e1 = (j + 2 < TSX) ? COL(RC, j + 2) : er;
+      if (EDGE) {
+        n = top ? t : n;
+        s = bot ? t : s;
+        w0 = (S.lmask >> j) & 1u ? t.x : w0;
+        e0 = (S.rmask >> j) & 1u ? t.x : e0;
+        w1 = (S.lmask >> (j + 1)) & 1u ? t.y : w1;
+        e1 = (S.rmask >> (j + 1)) & 1u ? t.y : e1;
+      }
+      if (j + 1 < TSX) {
+        const float2 m2 = make_float2(-2.0f, -2.0f);
+        const float2 m1 = make_float2(-1.0f, -1.0f);
+        const float2 ns = __ffma2_rn(m2, t, __fadd2_rn(n, s));
+        const float2 ew = __ffma2_rn(m2, t, make_float2(__fadd_rn(e0, w0), __fadd_rn(e1, w1)));
+        float2 d = __ffma2_rn(ns, k2.ry1, pw[q]);
+        d = __ffma2_rn(ew, k2.rx1, d);
+        const float2 z = __ffma2_rn(t, m1, k2.amb);  // amb - t, one rounding
+        d = __ffma2_rn(z, k2.rz1, d);
+        nv[q] = __ffma2_rn(k2.sdc, d, t);
+      } else {  // odd TSX: scalar last column
+        nv[q] = make_float2(HS_STEP(t.x, n.x, s.x, e0, w0, pw[q].x, kk.sdc, kk.rx1, kk.ry1, kk.rz1, kk.amb),
+                            0.f);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) cur[q] = nv[q];
+  }
+  // cur = level nsteps at row i - nsteps
+  const int ro = i - (FULL ? TT : S.nsteps);
+  float v[TSX];
+#pragma unroll
+  for (int j = 0; j < TSX; ++j) v[j] = COL(cur, j);
+  // direct (aligned) vector stores of the output row
+  if (ro >= S.y0 && ro < S.y1) {
+    float* orow = S.out + (size_t)ro * GW;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {
+      if ((S.omask >> c) & 1u) {
+        float* p = orow + S.csrc[c];
+#if CW == 4
+        *reinterpret_cast<float4*>(p) = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+#elif CW == 2
+        *reinterpret_cast<float2*>(p) = make_float2(v[2 * c], v[2 * c + 1]);
+#else
+        *p = v[c];
+#endif
+      }
+    }
+  }
+}
+
+template <bool EDGE, bool FULL>
+__device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
+  const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
+                make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
+  float2 R[TT][3][NP2];
+#pragma unroll
+  for (int a = 0; a < TT; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
+  float2 cur[NP2];
+  float wls[TT], ers[TT];
+  for (int i = S.ia; i <= S.ib; i += 3) {
+    hs_stream_iter<0, EDGE, FULL>(S, R, i, cur, wls, ers, kk, k2);
+    if (i + 1 > S.ib) break;
+    hs_stream_iter<1, EDGE, FULL>(S, R, i + 1, cur, wls, ers, kk, k2);
+    if (i + 2 > S.ib) break;
+    hs_stream_iter<2, EDGE, FULL>(S, R, i + 2, cur, wls, ers, kk, k2);
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(NTHREADS)
+hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
+               const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
+               float rz1, float amb) {
+  extern __shared__ __align__(128) float smem[];
+  const int tid = threadIdx.y * BSX + threadIdx.x;
+  const int wid = tid >> 5;
+  const int g = (int)blockIdx.x * WPB + wid;
+  if (g >= NSTRIPS * NSEGS) return;  // whole warp; no block barrier follows
+  HsStream S;
+  S.lane = tid & 31;
+  const int strip = g % NSTRIPS, seg = g / NSTRIPS;
+  S.tin = tin;
+  S.power = power;
+  S.out = out;
+  S.tring = smem + wid * WARP_FLOATS;
+  S.pring = S.tring + NR * SW;
+  S.gx0 = strip * UW - TA;
+  S.nsteps = nsteps;
+  S.y0 = seg * SEGH;
+  S.y1 = min(S.y0 + SEGH, GH);
+  S.ia = max(0, S.y0 - nsteps);
+  S.ib = S.y1 - 1 + nsteps;
+  S.omask = S.lmask = S.rmask = 0u;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const int wc = S.lane * TSX + c * CW;  // window column of the chunk
+    const int gx = S.gx0 + wc;
+    const bool in = gx >= 0 && gx < GW;   // chunks never straddle the grid edge (GW % 4 == 0)
+    S.cbytes[c] = in ? 4 * CW : 0;
+    S.csrc[c] = in ? gx : 0;
+    if (wc >= TA && wc < TA + UW && gx < GW) S.omask |= 1u << c;
+  }
+#pragma unroll
+  for (int j = 0; j < TSX; ++j) {
+    const int gx = S.gx0 + S.lane * TSX + j;
+    if (gx == 0) S.lmask |= 1u << j;
+    if (gx == GW - 1) S.rmask |= 1u << j;
+  }
+  for (int r = S.ia; r < S.ia + NR - 1; ++r) hs_stage_row(S, r);
+  const HsCoef kk{sdc, rx1, ry1, rz1, amb};
+  const bool edge = S.gx0 <= 0 || S.gx0 + SW > GW - 1 || S.ia == 0 || S.ib >= GH - 1;
+  // the full-depth launches (nsteps == TT) run a static level loop; only the
+  // remainder launch of ceil(20/TT) takes the dynamic one
+  if (nsteps == TT) {
+    if (edge)
+      hs_stream_run<true, true>(S, kk);
+    else
+      hs_stream_run<false, true>(S, kk);
+  } else {
+    if (edge)
+      hs_stream_run<true, false>(S, kk);
+    else
+      hs_stream_run<false, false>(S, kk);
+  }
+  cp_wait<0>();  // no copy may land in smem after the warp has left
+}
+
+#else  // !HS_STREAM
+
 #define OW (BSX * TSX)
 #define OH (BSY * TSY)
 #define EW (OW + 2 * TT)
@@ -92,10 +440,6 @@
 #define HS_BUF (BSY * SSS)
 #define HS_GUARD (EW + 1)
 #endif
-
-struct HsCoef {
-  float sdc, rx1, ry1, rz1, amb;
-};
 
 #if HS_REGISTER_MODE
 
@@ -382,6 +726,8 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   }
 #endif
 }
+
+#endif  // HS_STREAM
 
 #endif  // REFERENCE_ONLY
 

@@ -296,11 +296,53 @@ class Hotspot(Problem):
     def config_defines(self, cfg: dict) -> dict:
         return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
-                    UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"])
+                    UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"],
+                    HS_STREAM=int(self.stream_geometry(cfg) is not None))
 
-    @staticmethod
-    def kernel_mode(cfg: dict) -> tuple:
+    # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
+    STREAM_NR = 4            # bulk-copy ring depth (rows)
+    STREAM_SMEM_MAX = 200 * 1024
+    STREAM_REG_BASE = 56     # addresses, masks, coefficients, temporaries
+
+    def stream_geometry(self, cfg: dict) -> dict | None:
+        """Warp-streaming geometry, or None when the config does not fit it.
+
+        Mirrors the SW/TA/UW/SEGH/WARP_FLOATS macros of kernels/hotspot.cu:
+        register estimate 3*TT*TSX (level rings) + 4*TSX + 2*TT (prefetched
+        shuffles) must fit the
+        __launch_bounds__ budget, per-block smem the 200 KiB cap.
+        """
+        bx, by = cfg["block_size_x"], cfg["block_size_y"]
+        tsx, tsy = cfg["tile_size_x"], cfg["tile_size_y"]
+        t, shp = cfg["temporal_tiling_factor"], cfg["sh_power"]
+        nthreads = bx * by
+        if self.W % 4 or nthreads % 32:
+            return None
+        budget = min(255, 65536 // nthreads)
+        if 3 * t * tsx + 4 * tsx + 2 * t + self.STREAM_REG_BASE > budget:
+            return None
+        sw = 32 * tsx
+        ta = (t + 3) & ~3
+        uw = ((sw - ta - t) // 4) * 4
+        if uw < 4:
+            return None
+        segh = 32 * tsy
+        nr = self.STREAM_NR
+        pr = (8 if t + nr <= 8 else 16) if shp else 0
+        wpb = nthreads // 32
+        warp_floats = sw * (nr + pr)
+        smem = 4 * wpb * warp_floats
+        if smem > self.STREAM_SMEM_MAX:
+            return None
+        nstrips = -(-self.W // uw)
+        nsegs = -(-self.H // segh)
+        return dict(sw=sw, ta=ta, uw=uw, segh=segh, wpb=wpb, smem=smem, nstrips=nstrips,
+                    nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb))
+
+    def kernel_mode(self, cfg: dict) -> tuple:
         """(mode, floats per buffer, guard floats, buffers) -- mirrors kernels/hotspot.cu macros."""
+        if self.stream_geometry(cfg) is not None:
+            return "stream", 0, 0, 0
         bx, by = cfg["block_size_x"], cfg["block_size_y"]
         t, shp = cfg["temporal_tiling_factor"], cfg["sh_power"]
         ew = bx * cfg["tile_size_x"] + 2 * t
@@ -323,6 +365,9 @@ class Hotspot(Problem):
         # window buffers (the space's own smem model is (2 + sh_power) x
         # window, ts/spaces/hotspot.spec:25; we pad/skew them and add three
         # guard bands -- register mode keeps power in registers)
+        geo = self.stream_geometry(cfg)
+        if geo is not None:
+            return geo["smem"]
         _, buf, guard, nbuf = self.kernel_mode(cfg)
         return 4 * (nbuf * buf + 3 * guard)
 
@@ -349,9 +394,13 @@ class Hotspot(Problem):
         from .runtime import Launch
 
         plan = self.step_plan(cfg["temporal_tiling_factor"])
-        ow = cfg["block_size_x"] * cfg["tile_size_x"]
-        oh = cfg["block_size_y"] * cfg["tile_size_y"]
-        grid = (math.ceil(self.W / ow), math.ceil(self.H / oh), 1)
+        geo = self.stream_geometry(cfg)
+        if geo is not None:
+            grid = (geo["blocks"], 1, 1)  # warp tiles, strip-fastest
+        else:
+            ow = cfg["block_size_x"] * cfg["tile_size_x"]
+            oh = cfg["block_size_y"] * cfg["tile_size_y"]
+            grid = (math.ceil(self.W / ow), math.ceil(self.H / oh), 1)
         block = (cfg["block_size_x"], cfg["block_size_y"], 1)
         smem = self.smem_bytes(cfg)
         return self._chain(kernel, bufs, len(plan), lambda i, s, d: Launch(

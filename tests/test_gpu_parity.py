@@ -98,6 +98,40 @@ def test_full_size_answer_and_sweep(name, device):
         tgt.close()
 
 
+def _stream_configs(prob, n_per_t=4):
+    """Stream-mode configurations: every T, odd and even TSX, both sh_power values."""
+    names = prob.space.param_names
+    out = []
+    for c in stratified_sample(prob.space, 2000, seed=23, param="temporal_tiling_factor"):
+        d = dict(zip(names, c))
+        if prob.kernel_mode(d)[0] == "stream":
+            key = (d["temporal_tiling_factor"], d["tile_size_x"] % 2, d["sh_power"])
+            if sum(1 for o in out if o[0] == key) < 2:
+                out.append((key, c))
+    return [c for _, c in out]
+
+
+def test_hotspot_stream_mode_bit_exact(device):
+    """Warp-streaming hotspot (TMA bulk rows, shuffles, register level rings):
+    every T (incl. the remainder launch of 20 % T), odd/even TSX, power in
+    smem or through L1, grid edges -- bit-exact vs the C oracle."""
+    prob = Hotspot(width=520, height=264, iterations=20)
+    want = K.answer(prob)
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        configs = _stream_configs(prob)
+        assert len(configs) >= 30
+        for c in configs:
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+            st, out = tgt.run_output(c)
+            assert st is Status.OK, (c, out)
+            diff = int(np.sum(out != want))
+            assert diff == 0, f"stream {c}: {diff} elements differ"
+    finally:
+        tgt.close()
+
+
 def test_failure_mapping(device):
     from paper_2407_11488_b200 import runtime as rt
 

@@ -1,0 +1,53 @@
+"""Host-side geometry of the warp-streaming hotspot kernel (no GPU).
+
+Mirrors the invariants kernels/hotspot.cu relies on (HS_STREAM): bulk
+copies and stores need 16-byte aligned window origins and widths, the
+useful columns must lie inside the cells that stay valid for TT levels,
+strips and segments must tile the grid, and smem must fit.
+"""
+
+import numpy as np
+
+from paper_2407_11488_b200.problems import Hotspot
+from paper_2407_11488_b200.sweep import stratified_sample
+
+
+def test_stream_geometry_invariants():
+    prob = Hotspot()
+    names = prob.space.param_names
+    n_stream = 0
+    for c in stratified_sample(prob.space, 3000, seed=3, param="temporal_tiling_factor"):
+        d = dict(zip(names, c))
+        g = prob.stream_geometry(d)
+        mode = prob.kernel_mode(d)[0]
+        assert (g is not None) == (mode == "stream")
+        if g is None:
+            continue
+        n_stream += 1
+        t = d["temporal_tiling_factor"]
+        assert g["sw"] == 32 * d["tile_size_x"]
+        assert g["ta"] % 4 == 0 and g["uw"] % 4 == 0 and g["uw"] >= 4
+        assert g["ta"] >= t and g["ta"] + g["uw"] <= g["sw"] - t  # useful cells valid after t levels
+        assert g["nstrips"] * g["uw"] >= prob.W and (g["nstrips"] - 1) * g["uw"] < prob.W
+        assert g["nsegs"] * g["segh"] >= prob.H
+        assert g["blocks"] * g["wpb"] >= g["nstrips"] * g["segh"] // g["segh"] * g["nsegs"]
+        assert (g["sw"] * 4) % 16 == 0  # bulk-copy row size
+        assert g["smem"] <= Hotspot.STREAM_SMEM_MAX
+        assert prob.smem_bytes(d) == g["smem"]
+        lau = prob.launches(d, None, {k: _Fake() for k in ("temp", "tmp", "out", "power")})
+        assert lau[0].grid == (g["blocks"], 1, 1)
+    assert n_stream > 1000
+
+
+def test_stream_mode_needs_aligned_width():
+    d = dict(block_size_x=32, block_size_y=4, tile_size_x=4, tile_size_y=4, temporal_tiling_factor=6,
+             loop_unroll_factor_t=6, sh_power=1)
+    assert Hotspot(width=4096, height=64).kernel_mode(d)[0] == "stream"
+    assert Hotspot(width=4094, height=64).kernel_mode(d)[0] != "stream"
+    # too many registers for a 1024-thread block -> block-tile modes
+    big = dict(d, block_size_x=1024, block_size_y=1, tile_size_x=4)
+    assert Hotspot().kernel_mode(big)[0] != "stream"
+
+
+class _Fake:
+    ptr = 0
