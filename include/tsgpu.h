@@ -129,6 +129,10 @@ int tsg_set_max_dynamic_smem(tsg_kernel* fn, int bytes);
  * maximum, 0..100): kernels that stage tiles in smem ask for 100 so the
  * occupancy is not capped by a small default carveout. */
 int tsg_set_smem_carveout(tsg_kernel* fn, int percent);
+/* Resident blocks per SM for a launch shape (cuOccupancyMaxActive-
+ * BlocksPerMultiprocessor): lets a host size its grid in whole waves
+ * (the hotspot stream kernel picks its row-segment count from it). */
+int tsg_occupancy(tsg_kernel* fn, int block_threads, int dyn_smem, int* blocks_per_sm);
 
 /* Device memory ------------------------------------------------------------ */
 int tsg_alloc(tsg_ctx* ctx, size_t bytes, uint64_t* dptr);

@@ -39,6 +39,7 @@
   X(cuModuleGetGlobal) \
   X(cuModuleLoadData) \
   X(cuModuleUnload) \
+  X(cuOccupancyMaxActiveBlocksPerMultiprocessor) \
   X(cuStreamCreate) \
   X(cuStreamDestroy) \
   X(cuStreamSynchronize) \
@@ -100,6 +101,8 @@ inline const char* tsg_load_driver() {
 #define cuEventQuery (tsg_drv().p_cuEventQuery)
 #undef cuEventRecord
 #define cuEventRecord (tsg_drv().p_cuEventRecord)
+#undef cuOccupancyMaxActiveBlocksPerMultiprocessor
+#define cuOccupancyMaxActiveBlocksPerMultiprocessor (tsg_drv().p_cuOccupancyMaxActiveBlocksPerMultiprocessor)
 #undef cuFuncGetAttribute
 #define cuFuncGetAttribute (tsg_drv().p_cuFuncGetAttribute)
 #undef cuFuncSetAttribute

@@ -445,6 +445,15 @@ int tsg_set_smem_carveout(tsg_kernel* k, int percent) {
   return TSG_OK;
 }
 
+int tsg_occupancy(tsg_kernel* k, int block_threads, int dyn_smem, int* blocks_per_sm) {
+  if (!k || !blocks_per_sm) return fail(TSG_ERR_ARG, "null kernel/output");
+  int s = make_current(k->mod ? k->mod->ctx : nullptr);
+  if (s) return s;
+  CUresult r = cuOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k->fn, block_threads, (size_t)dyn_smem);
+  if (r != CUDA_SUCCESS) return fail(TSG_ERR_INVALID, "occupancy query: " + cu_msg(r));
+  return TSG_OK;
+}
+
 int tsg_alloc(tsg_ctx* c, size_t bytes, uint64_t* dptr) {
   int s = make_current(c);
   if (s) return s;

@@ -55,8 +55,10 @@ struct HsCoef {
 //
 // The unit of work is a WARP, not a block: warp w streams down a strip of
 // SW = 32*TSX window columns (lane L owns the TSX contiguous columns
-// L*TSX..L*TSX+TSX-1) and produces the UW useful columns of SEGH = 32*TSY
-// output rows.  The nsteps <= TT time levels are pipelined along the stream
+// L*TSX..L*TSX+TSX-1) and produces the UW useful columns of a segment of
+// `segh` output rows.  The host sizes segments from the kernel's measured
+// occupancy so the grid is TSY whole waves (TSY = 1: one wave, the
+// tallest segments, least vertical halo).  The nsteps <= TT time levels are pipelined along the stream
 // (time skewing): when input row i arrives, level k is advanced at row
 // i-k for k = 1..nsteps, so every level keeps only a 3-row ring in
 // registers (R[k][3][.]) and level nsteps leaves the pipeline one row per
@@ -64,7 +66,7 @@ struct HsCoef {
 // edge columns by warp shuffles (2 SHFL per lane per level): no block
 // barrier and no shared-memory exchange.  Halo cost: the strip recomputes
 // TA+TT columns (UW = floor4(SW - TA - TT) useful) and each segment streams
-// SEGH + 2*nsteps rows.
+// segh + 2*nsteps rows.
 //
 // Memory: every lane stages ITS OWN columns, so no lane ever waits for
 // another: input rows arrive by cp.async (LDGSTS, 16/8/4-byte chunks,
@@ -80,28 +82,34 @@ struct HsCoef {
 // identical to HS_STEP (bit-exact).
 //
 // loop_unroll_factor_t: the level loop is always fully unrolled (its
-// registers are indexed by level); the row stream is unrolled by 3 (ring
-// phases).  Mapping of the tunables: block = (BSX, BSY) threads = WPB warps
+// registers are indexed by level); UNROLL == 1 streams one row per
+// iteration (3-slot register rings, 3 ring phases), UNROLL > 1 two rows
+// per iteration (two independent chains per level, 4-slot rings, 2 phases).  Mapping of the tunables: block = (BSX, BSY) threads = WPB warps
 // taking consecutive warp tiles (strip-fastest), TSX = columns per lane,
-// TSY = output rows per lane / 32, TT = levels per launch.
+// TSY = waves of warp tiles (row segments per strip = TSY x the count that
+// fills one wave), TT = levels per launch.
 // ============================================================================
 
 #define SW (32 * TSX)
 #define TA (((TT) + 3) & ~3)
 #define UW (((SW - TA - TT) / 4) * 4)
-#define SEGH (32 * TSY)
 #define NSTRIPS ((GW + UW - 1) / UW)
-#define NSEGS ((GH + SEGH - 1) / SEGH)
 #define NTHREADS (BSX * BSY)
 #define WPB (NTHREADS / 32)
-#define NR 4
-// power ring: a power of two >= TT + NR rows (slot = row & (PR - 1))
-#define PR (SH_POWER ? ((TT + NR) <= 8 ? 8 : 16) : 0)
+// input ring: NR rows = NG groups of 2 rows (one group per iteration),
+// NG-1 groups in flight
+#define NR 8
+#define NG (NR / 2)
+// power ring: a power of two >= TT + NR + 2 rows (slot = row & (PR - 1))
+#define PR (SH_POWER ? ((TT + NR + 2) <= 16 ? 16 : 32) : 0)
 #define WARP_FLOATS (SW * (NR + PR))
 // staging chunk (floats) and chunks per lane
 #define CW ((TSX % 4) == 0 ? 4 : ((TSX % 2) == 0 ? 2 : 1))
 #define NCH (TSX / CW)
 #define NP2 ((TSX + 1) / 2)
+// rows per stream iteration: loop_unroll_factor_t > 1 unrolls the row stream
+// by two (two independent update chains per level)
+#define HS_RPI ((UNROLL) > 1 ? 2 : 1)
 #define COL(v, j) ((j) % 2 == 0 ? (v)[(j) / 2].x : (v)[(j) / 2].y)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -166,8 +174,7 @@ __device__ __forceinline__ void lds_pairs(float2 (&v)[NP2], const float* row, in
   for (int q = 0; q < NP2; ++q) v[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
 }
 
-// stage input (and power) row `row` into the rings; always commits a group
-// so that group counting stays uniform
+// stage input (and power) row `row` into the rings (no commit)
 __device__ __forceinline__ void hs_stage_row(const HsStream& S, int row) {
   if (row <= S.ib && row < GH) {
     const size_t rb = (size_t)row * GW;
@@ -180,120 +187,89 @@ __device__ __forceinline__ void hs_stage_row(const HsStream& S, int row) {
     for (int c = 0; c < NCH; ++c) cp_chunk(chunk_ptr(pr, c, S.lane), S.power + rb + S.csrc[c], S.cbytes[c]);
 #endif
   }
+}
+
+// rows (row, row+1) as one cp.async group -- always committed, so that the
+// group count stays uniform
+__device__ __forceinline__ void hs_stage_pair(const HsStream& S, int row) {
+  hs_stage_row(S, row);
+  hs_stage_row(S, row + 1);
   cp_commit();
 }
 
-// Fetch the operands of iteration i: its input row (landed by cp.async)
-// and the E/W neighbours of every level's centre row (level k-1 row i-k,
-// all computed by earlier iterations) -- all shuffled in ONE convergence
-// block, so the level chain that follows is straight-line code.  (Issuing
-// this at the end of iteration i-1 instead was measured slower.)
-template <int PH>
-__device__ __forceinline__ void hs_fetch(const HsStream& S, const float2 (&R)[TT][3][NP2], int i,
-                                         float2 (&cur)[NP2], float (&wls)[TT], float (&ers)[TT]) {
-  hs_stage_row(S, i + NR - 1);  // keep NR-1 rows in flight
-  cp_wait<NR - 1>();            // this lane's chunks of row i have landed
-  lds_pairs(cur, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
+__device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, int r) {
+#if SH_POWER
+  lds_pairs(pw, S.pring + ((r - S.ia) & (PR - 1)) * SW, S.lane);
+#else
+  const float* prow = S.power + (size_t)min(max(r, 0), GH - 1) * GW;
+  float t[TSX];
 #pragma unroll
-  for (int k = 1; k <= TT; ++k) {
-    const int sC = ((PH - k) % 3 + 3) % 3;
-    wls[k - 1] = __shfl_up_sync(0xffffffffu, COL(R[k - 1][sC], TSX - 1), 1);
-    ers[k - 1] = __shfl_down_sync(0xffffffffu, R[k - 1][sC][0].x, 1);
+  for (int c = 0; c < NCH; ++c) {
+    const float* p = prow + S.csrc[c];
+#if CW == 4
+    const float4 q = __ldg(reinterpret_cast<const float4*>(p));
+    t[4 * c] = q.x; t[4 * c + 1] = q.y; t[4 * c + 2] = q.z; t[4 * c + 3] = q.w;
+#elif CW == 2
+    const float2 q = __ldg(reinterpret_cast<const float2*>(p));
+    t[2 * c] = q.x; t[2 * c + 1] = q.y;
+#else
+    t[c] = __ldg(p);
+#endif
+  }
+#pragma unroll
+  for (int q = 0; q < NP2; ++q) pw[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
+#endif
+}
+
+// One cell-pair row update (HS_STEP on columns 2q, 2q+1; bit-exact):
+// C = centre row, N/S rows, wl/er = W of column 0 / E of column TSX-1
+// (from the neighbour lanes), P = power row.
+template <bool EDGE>
+__device__ __forceinline__ void hs_row_update(float2 (&nv)[NP2], const float2* N, const float2* Cc,
+                                              const float2* Sr, float wl, float er, const float2 (&P)[NP2],
+                                              bool top, bool bot, const HsStream& S, const HsCoef& kk,
+                                              const HsK2& k2) {
+#pragma unroll
+  for (int q = 0; q < NP2; ++q) {
+    const int j = 2 * q;
+    const float2 t = Cc[q];
+    float2 n = N[q], s = Sr[q];
+    // west / east neighbours of columns j and j+1 straddle the register
+    // pairs: form them as scalars and add them with two scalar FADDs (the
+    // FMA-pipe cost of one FADD2) instead of moving registers into pairs
+    float w0 = (j == 0) ? wl : COL(Cc, j - 1);
+    float e0 = (j + 1 < TSX) ? t.y : er;
+    float w1 = t.x;
+    float e1 = (j + 2 < TSX) ? COL(Cc, j + 2) : er;
+    if (EDGE) {
+      n = top ? t : n;
+      s = bot ? t : s;
+      w0 = (S.lmask >> j) & 1u ? t.x : w0;
+      e0 = (S.rmask >> j) & 1u ? t.x : e0;
+      w1 = (S.lmask >> (j + 1)) & 1u ? t.y : w1;
+      e1 = (S.rmask >> (j + 1)) & 1u ? t.y : e1;
+    }
+    if (j + 1 < TSX) {
+      const float2 m2 = make_float2(-2.0f, -2.0f);
+      const float2 m1 = make_float2(-1.0f, -1.0f);
+      const float2 ns = __ffma2_rn(m2, t, __fadd2_rn(n, s));
+      const float2 ew = __ffma2_rn(m2, t, make_float2(__fadd_rn(e0, w0), __fadd_rn(e1, w1)));
+      float2 d = __ffma2_rn(ns, k2.ry1, P[q]);
+      d = __ffma2_rn(ew, k2.rx1, d);
+      const float2 z = __ffma2_rn(t, m1, k2.amb);  // amb - t, one rounding
+      d = __ffma2_rn(z, k2.rz1, d);
+      nv[q] = __ffma2_rn(k2.sdc, d, t);
+    } else {  // odd TSX: scalar last column
+      nv[q] = make_float2(HS_STEP(t.x, n.x, s.x, e0, w0, P[q].x, kk.sdc, kk.rx1, kk.ry1, kk.rz1, kk.amb), 0.f);
+    }
   }
 }
 
-// One stream iteration: input row i (in cur) advances level k at row i-k.
-// PH = (i - ia) mod 3 fixes every register-ring slot at compile time.
-template <int PH, bool EDGE, bool FULL>
-__device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT][3][NP2], int i,
-                                               float2 (&cur)[NP2], float (&wls)[TT], float (&ers)[TT],
-                                               const HsCoef& kk, const HsK2& k2) {
-  const int lane = S.lane;
-  hs_fetch<PH>(S, R, i, cur, wls, ers);
-#pragma unroll
-  for (int k = 1; k <= TT; ++k) {
-    if (!FULL && k > S.nsteps) break;  // FULL: nsteps == TT (static: no exit phis)
-    const int r = i - k;  // row produced at level k
-    // ring slots of level k-1 rows r-1, r, r+1 (static after unrolling)
-    const int sN = ((PH - k - 1) % 3 + 3) % 3;
-    const int sC = ((PH - k) % 3 + 3) % 3;
-    const int sS = ((PH - k + 1) % 3 + 3) % 3;
-#pragma unroll
-    for (int q = 0; q < NP2; ++q) R[k - 1][sS][q] = cur[q];  // level k-1 row r+1
-    const float2* RN = R[k - 1][sN];
-    const float2* RC = R[k - 1][sC];
-    const float wl = wls[k - 1], er = ers[k - 1];
-    float2 pw[NP2];
-#if SH_POWER
-    lds_pairs(pw, S.pring + ((r - S.ia) & (PR - 1)) * SW, lane);
-#else
-    {
-      const float* prow = S.power + (size_t)min(max(r, 0), GH - 1) * GW;
-      float t[TSX];
-#pragma unroll
-      for (int c = 0; c < NCH; ++c) {
-        const float* p = prow + S.csrc[c];
-#if CW == 4
-        const float4 q = __ldg(reinterpret_cast<const float4*>(p));
-        t[4 * c] = q.x; t[4 * c + 1] = q.y; t[4 * c + 2] = q.z; t[4 * c + 3] = q.w;
-#elif CW == 2
-        const float2 q = __ldg(reinterpret_cast<const float2*>(p));
-        t[2 * c] = q.x; t[2 * c + 1] = q.y;
-#else
-        t[c] = __ldg(p);
-#endif
-      }
-#pragma unroll
-      for (int q = 0; q < NP2; ++q) pw[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
-    }
-#endif
-    const bool top = EDGE && (r == 0), bot = EDGE && (r == GH - 1);
-    float2 nv[NP2];
-#pragma unroll
-    for (int q = 0; q < NP2; ++q) {
-      const int j = 2 * q;
-      const float2 t = RC[q];
-      float2 n = RN[q], s = cur[q];
-      // west / east neighbours of columns j and j+1 straddle the register
-      // pairs: form them as scalars and add them with two scalar FADDs
-      // (the FMA pipe cost of one FADD2) instead of moving registers
-      float w0 = (j == 0) ? wl : COL(RC, j - 1);
-      float e0 = (j + 1 < TSX) ? t.y : er;
-      float w1 = t.x;
-      float e1 = (j + 2 < TSX) ? COL(RC, j + 2) : er;
-      if (EDGE) {
-        n = top ? t : n;
-        s = bot ? t : s;
-        w0 = (S.lmask >> j) & 1u ? t.x : w0;
-        e0 = (S.rmask >> j) & 1u ? t.x : e0;
-        w1 = (S.lmask >> (j + 1)) & 1u ? t.y : w1;
-        e1 = (S.rmask >> (j + 1)) & 1u ? t.y : e1;
-      }
-      if (j + 1 < TSX) {
-        const float2 m2 = make_float2(-2.0f, -2.0f);
-        const float2 m1 = make_float2(-1.0f, -1.0f);
-        const float2 ns = __ffma2_rn(m2, t, __fadd2_rn(n, s));
-        const float2 ew = __ffma2_rn(m2, t, make_float2(__fadd_rn(e0, w0), __fadd_rn(e1, w1)));
-        float2 d = __ffma2_rn(ns, k2.ry1, pw[q]);
-        d = __ffma2_rn(ew, k2.rx1, d);
-        const float2 z = __ffma2_rn(t, m1, k2.amb);  // amb - t, one rounding
-        d = __ffma2_rn(z, k2.rz1, d);
-        nv[q] = __ffma2_rn(k2.sdc, d, t);
-      } else {  // odd TSX: scalar last column
-        nv[q] = make_float2(HS_STEP(t.x, n.x, s.x, e0, w0, pw[q].x, kk.sdc, kk.rx1, kk.ry1, kk.rz1, kk.amb),
-                            0.f);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NP2; ++q) cur[q] = nv[q];
-  }
-  // cur = level nsteps at row i - nsteps
-  const int ro = i - (FULL ? TT : S.nsteps);
-  float v[TSX];
-#pragma unroll
-  for (int j = 0; j < TSX; ++j) v[j] = COL(cur, j);
-  // direct (aligned) vector stores of the output row
+__device__ __forceinline__ void hs_store_row(const HsStream& S, int ro, const float2 (&cur)[NP2]) {
   if (ro >= S.y0 && ro < S.y1) {
+    float v[TSX];
+#pragma unroll
+    for (int j = 0; j < TSX; ++j) v[j] = COL(cur, j);
     float* orow = S.out + (size_t)ro * GW;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) {
@@ -311,8 +287,103 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
   }
 }
 
+// One stream iteration: input rows i, i+1 arrive; level k advances rows
+// a = i-k and b = i+1-k (two independent chains per level).  Level k-1
+// rows a-1, a live in the 4-slot register ring; rows a+1, a+2 are the
+// two fresh rows the previous level just produced (they then replace the
+// dead slots of rows a-3, a-2).  Slots: row x at (x - ia) & 3, static for
+// PH = ((i - ia) / 2) & 1.
+template <int PH, bool EDGE, bool FULL>
+__device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT][4][NP2], int i,
+                                               const HsCoef& kk, const HsK2& k2) {
+  hs_stage_pair(S, i + NR - 2);  // keep NG-1 row pairs in flight
+  cp_wait<NG - 1>();             // this lane's chunks of rows i, i+1 have landed
+  float2 f0[NP2], f1[NP2];       // fresh rows of the previous level (level 0: input)
+  lds_pairs(f0, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
+  lds_pairs(f1, S.tring + ((i + 1 - S.ia) & (NR - 1)) * SW, S.lane);
+  // E/W neighbours of every level's OLD centre row (level k-1 row a),
+  // hoisted into one convergence block
+  float wla[TT], era[TT];
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    const int sC = ((2 * PH - k) % 4 + 4) % 4;
+    wla[k - 1] = __shfl_up_sync(0xffffffffu, COL(R[k - 1][sC], TSX - 1), 1);
+    era[k - 1] = __shfl_down_sync(0xffffffffu, R[k - 1][sC][0].x, 1);
+  }
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    if (!FULL && k > S.nsteps) break;  // FULL: nsteps == TT (static: no exit phis)
+    const int a = i - k;
+    const int sN = ((2 * PH - k - 1) % 4 + 4) % 4;  // row a-1
+    const int sC = ((2 * PH - k) % 4 + 4) % 4;      // row a
+    const int s0 = ((2 * PH - k + 1) % 4 + 4) % 4;  // row a+1 (fresh f0)
+    const int s1 = ((2 * PH - k + 2) % 4 + 4) % 4;  // row a+2 (fresh f1)
+    // E/W of the fresh centre row a+1 (row b's centre)
+    const float wlb = __shfl_up_sync(0xffffffffu, COL(f0, TSX - 1), 1);
+    const float erb = __shfl_down_sync(0xffffffffu, f0[0].x, 1);
+    float2 pa[NP2], pb[NP2];
+    hs_power(pa, S, a);
+    hs_power(pb, S, a + 1);
+    float2 na[NP2], nb[NP2];
+    hs_row_update<EDGE>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, EDGE && a == 0,
+                        EDGE && a == GH - 1, S, kk, k2);
+    hs_row_update<EDGE>(nb, R[k - 1][sC], f0, f1, wlb, erb, pb, EDGE && a + 1 == 0, EDGE && a + 1 == GH - 1, S,
+                        kk, k2);
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) {
+      R[k - 1][s0][q] = f0[q];
+      R[k - 1][s1][q] = f1[q];
+      f0[q] = na[q];
+      f1[q] = nb[q];
+    }
+  }
+  // f0, f1 = level nsteps at rows i - nsteps, i + 1 - nsteps
+  const int ro = i - (FULL ? TT : S.nsteps);
+  hs_store_row(S, ro, f0);
+  hs_store_row(S, ro + 1, f1);
+}
+
+// ---- one row per iteration (loop_unroll_factor_t == 1) --------------------
+// Level k-1 keeps rows a-1, a in a 3-slot ring (row x at (x - ia) mod 3,
+// static for PH = (i - ia) mod 3); the fresh row a+1 arrives from level k-1.
+template <int PH, bool EDGE, bool FULL>
+__device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[TT][3][NP2], int i,
+                                                const HsCoef& kk, const HsK2& k2) {
+  hs_stage_row(S, i + NR - 1);  // keep NR-1 rows in flight (one group per row)
+  cp_commit();
+  cp_wait<NR - 1>();
+  float2 f0[NP2];
+  lds_pairs(f0, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
+  float wla[TT], era[TT];  // E/W of every level's centre row, one convergence block
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    const int sC = ((PH - k) % 3 + 3) % 3;
+    wla[k - 1] = __shfl_up_sync(0xffffffffu, COL(R[k - 1][sC], TSX - 1), 1);
+    era[k - 1] = __shfl_down_sync(0xffffffffu, R[k - 1][sC][0].x, 1);
+  }
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    if (!FULL && k > S.nsteps) break;
+    const int a = i - k;
+    const int sN = ((PH - k - 1) % 3 + 3) % 3;
+    const int sC = ((PH - k) % 3 + 3) % 3;
+    const int s0 = ((PH - k + 1) % 3 + 3) % 3;
+    float2 pa[NP2];
+    hs_power(pa, S, a);
+    float2 na[NP2];
+    hs_row_update<EDGE>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, EDGE && a == 0,
+                        EDGE && a == GH - 1, S, kk, k2);
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) {
+      R[k - 1][s0][q] = f0[q];
+      f0[q] = na[q];
+    }
+  }
+  hs_store_row(S, i - (FULL ? TT : S.nsteps), f0);
+}
+
 template <bool EDGE, bool FULL>
-__device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
+__device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& kk) {
   const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
                 make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
   float2 R[TT][3][NP2];
@@ -322,26 +393,43 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
     for (int b = 0; b < 3; ++b)
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
-  float2 cur[NP2];
-  float wls[TT], ers[TT];
   for (int i = S.ia; i <= S.ib; i += 3) {
-    hs_stream_iter<0, EDGE, FULL>(S, R, i, cur, wls, ers, kk, k2);
+    hs_stream_iter1<0, EDGE, FULL>(S, R, i, kk, k2);
     if (i + 1 > S.ib) break;
-    hs_stream_iter<1, EDGE, FULL>(S, R, i + 1, cur, wls, ers, kk, k2);
+    hs_stream_iter1<1, EDGE, FULL>(S, R, i + 1, kk, k2);
     if (i + 2 > S.ib) break;
-    hs_stream_iter<2, EDGE, FULL>(S, R, i + 2, cur, wls, ers, kk, k2);
+    hs_stream_iter1<2, EDGE, FULL>(S, R, i + 2, kk, k2);
+  }
+}
+
+// ---- two rows per iteration (loop_unroll_factor_t > 1) -----------------------
+template <bool EDGE, bool FULL>
+__device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
+  const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
+                make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
+  float2 R[TT][4][NP2];
+#pragma unroll
+  for (int a = 0; a < TT; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
+  for (int i = S.ia; i <= S.ib; i += 4) {
+    hs_stream_iter<0, EDGE, FULL>(S, R, i, kk, k2);
+    if (i + 2 > S.ib) break;
+    hs_stream_iter<1, EDGE, FULL>(S, R, i + 2, kk, k2);
   }
 }
 
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
                const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
-               float rz1, float amb) {
+               float rz1, float amb, int segh, int nsegs) {
   extern __shared__ __align__(128) float smem[];
   const int tid = threadIdx.y * BSX + threadIdx.x;
   const int wid = tid >> 5;
   const int g = (int)blockIdx.x * WPB + wid;
-  if (g >= NSTRIPS * NSEGS) return;  // whole warp; no block barrier follows
+  if (g >= NSTRIPS * nsegs) return;  // whole warp; no block barrier follows
   HsStream S;
   S.lane = tid & 31;
   const int strip = g % NSTRIPS, seg = g / NSTRIPS;
@@ -352,8 +440,8 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   S.pring = S.tring + NR * SW;
   S.gx0 = strip * UW - TA;
   S.nsteps = nsteps;
-  S.y0 = seg * SEGH;
-  S.y1 = min(S.y0 + SEGH, GH);
+  S.y0 = seg * segh;
+  S.y1 = min(S.y0 + segh, GH);
   S.ia = max(0, S.y0 - nsteps);
   S.ib = S.y1 - 1 + nsteps;
   S.omask = S.lmask = S.rmask = 0u;
@@ -372,21 +460,33 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
     if (gx == 0) S.lmask |= 1u << j;
     if (gx == GW - 1) S.rmask |= 1u << j;
   }
-  for (int r = S.ia; r < S.ia + NR - 1; ++r) hs_stage_row(S, r);
+#if HS_RPI == 2
+  for (int g2 = 0; g2 < NG - 1; ++g2) hs_stage_pair(S, S.ia + 2 * g2);
+#else
+  for (int r = S.ia; r < S.ia + NR - 1; ++r) {
+    hs_stage_row(S, r);
+    cp_commit();
+  }
+#endif
   const HsCoef kk{sdc, rx1, ry1, rz1, amb};
   const bool edge = S.gx0 <= 0 || S.gx0 + SW > GW - 1 || S.ia == 0 || S.ib >= GH - 1;
   // the full-depth launches (nsteps == TT) run a static level loop; only the
   // remainder launch of ceil(20/TT) takes the dynamic one
+#if HS_RPI == 2
+#define HS_RUN hs_stream_run
+#else
+#define HS_RUN hs_stream_run1
+#endif
   if (nsteps == TT) {
     if (edge)
-      hs_stream_run<true, true>(S, kk);
+      HS_RUN<true, true>(S, kk);
     else
-      hs_stream_run<false, true>(S, kk);
+      HS_RUN<false, true>(S, kk);
   } else {
     if (edge)
-      hs_stream_run<true, false>(S, kk);
+      HS_RUN<true, false>(S, kk);
     else
-      hs_stream_run<false, false>(S, kk);
+      HS_RUN<false, false>(S, kk);
   }
   cp_wait<0>();  // no copy may land in smem after the warp has left
 }

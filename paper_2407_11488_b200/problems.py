@@ -300,17 +300,21 @@ class Hotspot(Problem):
                     HS_STREAM=int(self.stream_geometry(cfg) is not None))
 
     # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
-    STREAM_NR = 4            # bulk-copy ring depth (rows)
+    STREAM_NR = 8            # cp.async input ring depth (rows; pairs per group)
     STREAM_SMEM_MAX = 200 * 1024
     STREAM_REG_BASE = 56     # addresses, masks, coefficients, temporaries
 
-    def stream_geometry(self, cfg: dict) -> dict | None:
+    def stream_geometry(self, cfg: dict, blocks_per_sm: int | None = None,
+                        n_sm: int = 148) -> dict | None:
         """Warp-streaming geometry, or None when the config does not fit it.
 
-        Mirrors the SW/TA/UW/SEGH/WARP_FLOATS macros of kernels/hotspot.cu:
-        register estimate 3*TT*TSX (level rings) + 4*TSX + 2*TT (prefetched
-        shuffles) must fit the
-        __launch_bounds__ budget, per-block smem the 200 KiB cap.
+        Mirrors the SW/TA/UW/WARP_FLOATS macros of kernels/hotspot.cu:
+        register estimate 3*TT*TSX (level rings) + 4*TSX + 2*TT (hoisted
+        shuffles) must fit the __launch_bounds__ budget, per-block smem the
+        200 KiB cap.  Row segments: TSY whole waves of warp tiles, one wave
+        = (resident blocks per SM x warps per block x SMs) tiles; the
+        resident count comes from the driver's occupancy query at launch
+        (``blocks_per_sm``), else from the register estimate.
         """
         bx, by = cfg["block_size_x"], cfg["block_size_y"]
         tsx, tsy = cfg["tile_size_x"], cfg["tile_size_y"]
@@ -319,25 +323,35 @@ class Hotspot(Problem):
         if self.W % 4 or nthreads % 32:
             return None
         budget = min(255, 65536 // nthreads)
-        if 3 * t * tsx + 4 * tsx + 2 * t + self.STREAM_REG_BASE > budget:
+        regs = 3 * t * tsx + 4 * tsx + 2 * t + self.STREAM_REG_BASE
+        if cfg["loop_unroll_factor_t"] > 1:  # two rows per iteration: second chain's temporaries
+            regs += 4 * tsx + 8
+        if regs > budget:
             return None
         sw = 32 * tsx
         ta = (t + 3) & ~3
         uw = ((sw - ta - t) // 4) * 4
         if uw < 4:
             return None
-        segh = 32 * tsy
         nr = self.STREAM_NR
-        pr = (8 if t + nr <= 8 else 16) if shp else 0
+        pr = (16 if t + nr + 2 <= 16 else 32) if shp else 0
         wpb = nthreads // 32
         warp_floats = sw * (nr + pr)
         smem = 4 * wpb * warp_floats
         if smem > self.STREAM_SMEM_MAX:
             return None
         nstrips = -(-self.W // uw)
+        if blocks_per_sm is None:  # estimate (CPU-side planning / tests)
+            per_warp = -(-min(regs, budget) * 32 // 256) * 256
+            by_regs = 65536 // per_warp // wpb
+            by_smem = (228 * 1024) // (smem + 1024) if smem else 32
+            blocks_per_sm = max(1, min(by_regs, by_smem, 32, 64 // wpb))
+        wave = max(1, blocks_per_sm * wpb * n_sm // nstrips)  # row segments per strip, one wave
+        nsegs = min(tsy * wave, -(-self.H // 8))
+        segh = -(-self.H // nsegs)
         nsegs = -(-self.H // segh)
         return dict(sw=sw, ta=ta, uw=uw, segh=segh, wpb=wpb, smem=smem, nstrips=nstrips,
-                    nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb))
+                    nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb), blocks_per_sm=blocks_per_sm)
 
     def kernel_mode(self, cfg: dict) -> tuple:
         """(mode, floats per buffer, guard floats, buffers) -- mirrors kernels/hotspot.cu macros."""
@@ -395,8 +409,14 @@ class Hotspot(Problem):
 
         plan = self.step_plan(cfg["temporal_tiling_factor"])
         geo = self.stream_geometry(cfg)
+        extra = []
         if geo is not None:
+            occ = getattr(kernel, "occupancy", None)
+            if occ is not None:  # size the row segments in whole waves of the real residency
+                bps = occ(cfg["block_size_x"] * cfg["block_size_y"], geo["smem"])
+                geo = self.stream_geometry(cfg, blocks_per_sm=max(1, bps), n_sm=kernel.sm_count)
             grid = (geo["blocks"], 1, 1)  # warp tiles, strip-fastest
+            extra = [C.c_int(geo["segh"]), C.c_int(geo["nsegs"])]
         else:
             ow = cfg["block_size_x"] * cfg["tile_size_x"]
             oh = cfg["block_size_y"] * cfg["tile_size_y"]
@@ -405,7 +425,7 @@ class Hotspot(Problem):
         smem = self.smem_bytes(cfg)
         return self._chain(kernel, bufs, len(plan), lambda i, s, d: Launch(
             kernel, grid, block, [_u64(d), _u64(s), _u64(bufs["power"]), C.c_int(plan[i])]
-            + self._coeff_args(), smem=smem))
+            + self._coeff_args() + extra, smem=smem))
 
     def reference_launches(self, kernel, bufs: dict) -> list:
         from .runtime import Launch

@@ -76,6 +76,7 @@ SIGNATURES = {
     "tsg_func_attrs": (C.c_int, [C.c_void_p] + [C.POINTER(C.c_int)] * 4),
     "tsg_set_max_dynamic_smem": (C.c_int, [C.c_void_p, C.c_int]),
     "tsg_set_smem_carveout": (C.c_int, [C.c_void_p, C.c_int]),
+    "tsg_occupancy": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_int)]),
     "tsg_alloc": (C.c_int, [C.c_void_p, C.c_size_t, C.POINTER(C.c_uint64)]),
     "tsg_free": (C.c_int, [C.c_void_p, C.c_uint64]),
     "tsg_h2d": (C.c_int, [C.c_void_p, C.c_uint64, C.c_void_p, C.c_size_t]),
@@ -248,6 +249,16 @@ class Kernel:
 
     def set_smem_carveout(self, percent: int) -> int:
         return self.module.dev.lib.tsg_set_smem_carveout(self.handle, int(percent))
+
+    def occupancy(self, block_threads: int, dyn_smem: int) -> int:
+        """Resident blocks per SM for this launch shape (0 if it cannot launch)."""
+        n = C.c_int(0)
+        rc = self.module.dev.lib.tsg_occupancy(self.handle, int(block_threads), int(dyn_smem), C.byref(n))
+        return n.value if rc == OK else 0
+
+    @property
+    def sm_count(self) -> int:
+        return int(self.module.dev.info["sm_count"])
 
 
 class Launch:

@@ -99,14 +99,16 @@ def test_full_size_answer_and_sweep(name, device):
 
 
 def _stream_configs(prob, n_per_t=4):
-    """Stream-mode configurations: every T, odd and even TSX, both sh_power values."""
+    """Stream-mode configurations: every T, odd and even TSX, both sh_power
+    values, one and two rows per iteration."""
     names = prob.space.param_names
     out = []
     for c in stratified_sample(prob.space, 2000, seed=23, param="temporal_tiling_factor"):
         d = dict(zip(names, c))
         if prob.kernel_mode(d)[0] == "stream":
-            key = (d["temporal_tiling_factor"], d["tile_size_x"] % 2, d["sh_power"])
-            if sum(1 for o in out if o[0] == key) < 2:
+            key = (d["temporal_tiling_factor"], d["tile_size_x"] % 2, d["sh_power"],
+                   d["loop_unroll_factor_t"] > 1)
+            if sum(1 for o in out if o[0] == key) < 1:
                 out.append((key, c))
     return [c for _, c in out]
 

@@ -30,7 +30,8 @@ def test_stream_geometry_invariants():
         assert g["ta"] >= t and g["ta"] + g["uw"] <= g["sw"] - t  # useful cells valid after t levels
         assert g["nstrips"] * g["uw"] >= prob.W and (g["nstrips"] - 1) * g["uw"] < prob.W
         assert g["nsegs"] * g["segh"] >= prob.H
-        assert g["blocks"] * g["wpb"] >= g["nstrips"] * g["segh"] // g["segh"] * g["nsegs"]
+        assert g["blocks"] * g["wpb"] >= g["nstrips"] * g["nsegs"]
+        assert g["segh"] * (g["nsegs"] - 1) < prob.H
         assert (g["sw"] * 4) % 16 == 0  # bulk-copy row size
         assert g["smem"] <= Hotspot.STREAM_SMEM_MAX
         assert prob.smem_bytes(d) == g["smem"]
