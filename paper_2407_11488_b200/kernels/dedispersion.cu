@@ -29,6 +29,240 @@ __constant__ float d_delay[NCH];
 #define STR2(x) #x
 #define STR(x) STR2(x)
 
+#if defined(DD_WIN) && DD_WIN
+// ============================================================================
+// WINDOW mode (host-selected for block_size_x == 32 with strided samples and
+// contiguous DMs): a warp's 32 lanes own consecutive samples (lane L:
+// s0 + L + 32*i, i < TSX) and ALL share the same TSY consecutive DMs, so
+// every shift is warp-uniform.  Adjacent DMs shift by 0 or 1 sample (the
+// sweep's slope is < 1 sample per DM), hence for one channel the TSY DMs
+// need only the SPAN+1 samples s + sh0 + k (k <= span <= SPAN) per owned
+// sample: a lane loads that small window once per channel (coalesced
+// 128-byte rows) and reuses every value for all DMs whose offset hits it --
+// TSY*TSX adds per TSX*(1+span) loads instead of one load per add.  The
+// increment pattern of the TSY shifts (TSY-1 bits) is warp-uniform: one
+// indirect branch per channel selects a straight-line block with static
+// register offsets.  Patterns (with sh0) are computed 32 channels at a time,
+// one channel per lane, and broadcast with a shuffle.  Packed FADD2 adds
+// sample pairs; channels are summed in ascending order (bit-exact).
+// ============================================================================
+#define W (SPAN + 1)
+#define NPAT (1 << (TSY - 1))
+#define XP ((TSX + 1) / 2)
+
+__host__ __device__ constexpr int dd_popc(int v) { return v ? (v & 1) + dd_popc(v >> 1) : 0; }
+// Dense case index of a pattern: patterns ordered by increment count
+// (span), then by value -- span 0 is index 0, span 1 are 1..TSY-1, ... --
+// so the dispatch can test the frequent small spans first (a switch is
+// lowered to a compare tree, never a jump table).  Only spans <= SPAN occur.
+__host__ __device__ constexpr int dd_before(int span, int p) {  // patterns < p with this span
+  return p == 0 ? 0 : dd_before(span, p - 1) + (dd_popc(p - 1) == span ? 1 : 0);
+}
+__host__ __device__ constexpr int dd_rank(int p) {
+  return dd_before(dd_popc(p), p) + (dd_popc(p) >= 1 ? dd_before(0, NPAT) : 0) +
+         (dd_popc(p) >= 2 ? dd_before(1, NPAT) : 0) + (dd_popc(p) >= 3 ? dd_before(2, NPAT) : 0) +
+         (dd_popc(p) >= 4 ? dd_before(3, NPAT) : 0) + (dd_popc(p) >= 5 ? dd_before(4, NPAT) : 0) +
+         (dd_popc(p) >= 6 ? dd_before(5, NPAT) : 0) + (dd_popc(p) >= 7 ? dd_before(6, NPAT) : 0);
+}
+__host__ __device__ constexpr int dd_nth(int n, int p = 0) {  // inverse of dd_rank
+  return p >= NPAT ? 0 : (dd_rank(p) == n ? p : dd_nth(n, p + 1));
+}
+// first dense index of each span
+#define DD_S1 1
+#define DD_S2 (DD_S1 + dd_before(1, NPAT))
+#define DD_S3 (DD_S2 + dd_before(2, NPAT))
+#define NVALID (DD_S3 + (SPAN >= 3 ? dd_before(3, NPAT) : 0))
+
+struct DdWin {
+  float2 acc[TSY][XP];
+};
+
+// one channel with increment pattern P (static): load exactly the popc(P)+1
+// window samples per owned sample and add them to the TSY DM accumulators
+template <int P>
+__device__ __forceinline__ void dd_accum(DdWin& st, const float* p) {
+  constexpr int span = dd_popc(P);
+  float2 x[XP][span + 1];
+#pragma unroll
+  for (int q = 0; q < XP; ++q)
+#pragma unroll
+    for (int k = 0; k <= span; ++k) {
+      x[q][k].x = p[64 * q + k];
+      x[q][k].y = (2 * q + 1 < TSX) ? p[64 * q + 32 + k] : 0.f;
+    }
+#pragma unroll
+  for (int j = 0; j < TSY; ++j) {
+    const int g = __popc(P & ((1 << j) - 1));  // offset of DM j (static after unrolling)
+#pragma unroll
+    for (int q = 0; q < XP; ++q) {
+      if (2 * q + 1 < TSX)
+        st.acc[j][q] = __fadd2_rn(st.acc[j][q], x[q][g]);
+      else
+        st.acc[j][q].x = __fadd_rn(st.acc[j][q].x, x[q][g].x);
+    }
+  }
+}
+
+// switch over dense indices LO .. LO+N-1; cases past N have empty bodies and
+// fold into `default`, so the compare tree only spans the N live cases
+#define DD_CASE(I)                                                 \
+  case I:                                                          \
+    if constexpr ((I) < N) dd_accum<dd_nth(LO + ((I) < N ? (I) : 0))>(st, p); \
+    break;
+#define DD_C4(I) DD_CASE(I) DD_CASE(I + 1) DD_CASE(I + 2) DD_CASE(I + 3)
+#define DD_C16(I) DD_C4(I) DD_C4(I + 4) DD_C4(I + 8) DD_C4(I + 12)
+
+template <int LO, int N>
+__device__ __forceinline__ void dd_switch(DdWin& st, int idx, const float* p) {
+  switch (idx - LO) {
+    DD_C16(0) DD_C16(16) DD_C16(32) DD_C16(48)
+    default:
+      break;
+  }
+}
+
+// frequency-ordered dispatch: span 0 (one pattern, ~1/4 of all channels),
+// span 1 (TSY-1 patterns, the most frequent), then spans 2 and 3
+__device__ __forceinline__ void dd_dispatch(DdWin& st, int idx, const float* p) {
+  if (idx == 0) {
+    dd_accum<0>(st, p);
+  } else if (SPAN < 2 || idx < DD_S2) {
+    dd_switch<DD_S1, (SPAN >= 1 ? DD_S2 - DD_S1 : 0)>(st, idx, p);
+  } else if (SPAN < 3 || idx < DD_S3) {
+    dd_switch<DD_S2, (SPAN >= 2 ? DD_S3 - DD_S2 : 0)>(st, idx, p);
+  } else {
+    dd_switch<DD_S3, NVALID - DD_S3>(st, idx, p);
+  }
+}
+
+// Shared-memory staging: per chunk of CC = 32 channels, each channel's
+// block-wide row segment (the block's 32*TSX samples shifted by the block's
+// FIRST DM, plus BLKSPAN + SPAN samples of DM spread, aligned down to 16 B)
+// is brought in by one TMA bulk copy (cp.async.bulk, issued by warp 0's
+// lanes, completion on the stage's mbarrier), NSTAGE chunks in flight.
+// Warps then read their windows with LDS: 32 consecutive floats at any
+// alignment are one conflict-free wavefront (an unaligned 128-byte global
+// load costs ~2.4 L1 wavefronts and an LSU queue slot).
+#define CC 32
+#define ROWLEN ((32 * TSX + BLKSPAN + SPAN + 4 + 3) & ~3)
+#define NSTAGE 3
+
+__device__ __forceinline__ unsigned dd_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void dd_mbar_init(unsigned long long* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dd_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void dd_mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void dd_mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(dd_smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void dd_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dd_smem_u32(dst)), "l"(src), "r"(bytes), "r"(dd_smem_u32(b))
+      : "memory");
+}
+
+// warp 0: stage chunk t (channels t*CC ..) into `stage`
+__device__ __forceinline__ void dd_issue_chunk(const float* __restrict__ in, float* stage, unsigned long long* bar,
+                                               int t, int sb, float dmb, int lane) {
+  const int ch = t * CC + lane;
+  const int nvalid = NCH - t * CC < CC ? NCH - t * CC : CC;
+  if (lane == 0) dd_mbar_expect(bar, (unsigned)(nvalid * ROWLEN * 4));
+  __syncwarp();
+  if (ch < NCH) {
+    const int shb = __float2int_rz(__fmul_rn(dmb, d_delay[ch]));
+    const int a = (sb + shb) & ~3;
+    dd_bulk(stage + lane * ROWLEN, in + (size_t)ch * IN_PITCH + a, ROWLEN * 4, bar);
+  }
+}
+
+extern "C" __global__ void __launch_bounds__(BSX * BSY)
+dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float dm_first,
+                    float dm_step) {
+  extern __shared__ __align__(128) float smem[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NSTAGE * CC * ROWLEN);
+  unsigned char* pidx = reinterpret_cast<unsigned char*>(bars + NSTAGE);  // pattern -> dense case
+  for (int p = threadIdx.y * 32 + threadIdx.x; p < NPAT; p += BSX * BSY) pidx[p] = (unsigned char)dd_rank(p);
+  const int lane = threadIdx.x;  // BSX == 32: one warp per DM group
+  const int w = threadIdx.y;
+  const int sb = (int)blockIdx.y * (32 * TSX);  // block's first sample
+  const int db0 = (int)blockIdx.x * (BSY * TSY);  // block's first DM (< NDM)
+  const int d0 = db0 + w * TSY;
+  const float dmb = __fadd_rn(dm_first, __fmul_rn((float)db0, dm_step));
+  if (w == 0 && lane == 0) {
+#pragma unroll
+    for (int b = 0; b < NSTAGE; ++b) dd_mbar_init(bars + b);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nchunks = (NCH + CC - 1) / CC;
+  if (w == 0)
+    for (int t = 0; t < NSTAGE && t < nchunks; ++t)
+      dd_issue_chunk(in, smem + t * CC * ROWLEN, bars + t, t, sb, dmb, lane);
+  DdWin st;
+#pragma unroll
+  for (int j = 0; j < TSY; ++j)
+#pragma unroll
+    for (int q = 0; q < XP; ++q) st.acc[j][q] = make_float2(0.f, 0.f);
+  for (int t = 0; t < nchunks; ++t) {
+    const int stg = t % NSTAGE;
+    // lane c: this warp's offset into channel t*CC+c's staged row and the
+    // increment pattern of its TSY shifts
+    int mine = 0;
+    {
+      const int ch = t * CC + lane < NCH ? t * CC + lane : NCH - 1;
+      const float dl = d_delay[ch];
+      // DM values recomputed per chunk (cheaper than 8 live registers);
+      // clamped overshoot rows compute a valid DM and are never stored
+      const int shb = __float2int_rz(__fmul_rn(dmb, dl));
+      const int sh0 = __float2int_rz(__fmul_rn(__fadd_rn(dm_first, __fmul_rn((float)min(d0, NDM - 1), dm_step)), dl));
+      int prev = sh0, pat = 0;
+#pragma unroll
+      for (int j = 1; j < TSY; ++j) {
+        const float dmj = __fadd_rn(dm_first, __fmul_rn((float)min(d0 + j, NDM - 1), dm_step));
+        const int shj = __float2int_rz(__fmul_rn(dmj, dl));
+        pat |= (shj - prev) << (j - 1);  // 0 or 1 (slope < 1 sample per DM)
+        prev = shj;
+      }
+      const int rel = sh0 - shb + ((sb + shb) & 3);  // offset from the aligned row start
+      mine = (rel << 8) | pidx[pat];
+    }
+    dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
+    const float* srow = smem + stg * CC * ROWLEN + lane;
+    const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c, srow += ROWLEN) {
+      const int pk = __shfl_sync(0xffffffffu, mine, c);
+      dd_dispatch(st, pk & 0xff, srow + (pk >> 8));
+    }
+    __syncthreads();  // every warp is done with this stage
+    if (w == 0 && t + NSTAGE < nchunks)
+      dd_issue_chunk(in, smem + stg * CC * ROWLEN, bars + stg, t + NSTAGE, sb, dmb, lane);
+  }
+  const int s0 = sb + lane;
+#pragma unroll
+  for (int j = 0; j < TSY; ++j) {
+    if (d0 + j >= NDM) continue;
+    float* o = out + (size_t)(d0 + j) * NSAMP;
+#pragma unroll
+    for (int q = 0; q < XP; ++q) {
+      const int sa = s0 + 64 * q, sbb = sa + 32;
+      if (sa < NSAMP) o[sa] = st.acc[j][q].x;
+      if (2 * q + 1 < TSX && sbb < NSAMP) o[sbb] = st.acc[j][q].y;
+    }
+  }
+}
+
+#else  // generic AMBER-style kernel
+
 extern "C" __global__ void __launch_bounds__(BSX * BSY)
 dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float dm_first,
                     float dm_step) {
@@ -72,6 +306,8 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       if (s[i] < NSAMP) o[s[i]] = acc[j][i];
   }
 }
+
+#endif  // DD_WIN
 
 #endif  // REFERENCE_ONLY
 

@@ -497,7 +497,9 @@ class Dedispersion(Problem):
         self.delay = dm_delay_table(channels, f_min_mhz, ch_bw_mhz, t_samp_s)
         self.max_shift = int(dm_shifts(self.delay, dms, self.dm_first, self.dm_step).max())
         self.in_w = samples + self.max_shift
-        self.pitch = ((samples + self.max_shift + 128 + 31) // 32) * 32
+        # slack: grid-overshoot reads of the generic kernel (128) and the
+        # window kernel's staged row segments (<= 32*4 + block DM spread + 8)
+        self.pitch = ((samples + self.max_shift + 640 + 31) // 32) * 32
         self.seed = seed
 
     def data(self) -> np.ndarray:
@@ -519,8 +521,67 @@ class Dedispersion(Problem):
         return dict(NCH=self.NCH, NSAMP=self.NSAMP, NDM=self.NDM, IN_PITCH=self.pitch)
 
     def config_defines(self, cfg: dict) -> dict:
-        return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
-                    TSY=cfg["tile_size_y"], STX=cfg["tile_stride_x"], STY=cfg["tile_stride_y"])
+        d = dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
+                 TSY=cfg["tile_size_y"], STX=cfg["tile_stride_x"], STY=cfg["tile_stride_y"])
+        span = self.window_span(cfg)
+        if span is not None:
+            d.update(DD_WIN=1, SPAN=span, BLKSPAN=self.block_span(cfg))
+        return d
+
+    DD_STAGES = 3  # kernels/dedispersion.cu NSTAGE
+    DD_CC = 32     # channels per stage
+
+    def block_span(self, cfg: dict) -> int:
+        """Max shift spread over one block's BSY*TSY DMs (window kernel BLKSPAN)."""
+        nd = cfg["block_size_y"] * cfg["tile_size_y"]
+        key = ("blk", nd, self.NCH, self.NDM, self.dm_first, self.dm_step)
+        if key not in Dedispersion._spans:
+            sh = dm_shifts(self.delay, self.NDM, self.dm_first, self.dm_step).astype(np.int64)
+            first = np.arange(0, self.NDM, nd)
+            last = np.minimum(first + nd - 1, self.NDM - 1)
+            Dedispersion._spans[key] = int((sh[last] - sh[first]).max())
+        return Dedispersion._spans[key]
+
+    def smem_bytes(self, cfg: dict) -> int:
+        span = self.window_span(cfg)
+        if span is None:
+            return 0
+        rowlen = (32 * cfg["tile_size_x"] + self.block_span(cfg) + span + 4 + 3) & ~3
+        npat = 1 << (cfg["tile_size_y"] - 1)
+        return 4 * self.DD_STAGES * self.DD_CC * rowlen + 8 * self.DD_STAGES + npat
+
+    _spans: dict = {}
+
+    def _group_span(self, tsy: int) -> tuple:
+        """(max increment between adjacent DMs, max shift span of a TSY-DM group)."""
+        key = (tsy, self.NCH, self.NDM, self.dm_first, self.dm_step)
+        if key not in Dedispersion._spans:
+            sh = dm_shifts(self.delay, self.NDM, self.dm_first, self.dm_step).astype(np.int64)
+            n = -(-self.NDM // tsy) * tsy
+            idx = np.minimum(np.arange(n), self.NDM - 1)  # overshoot rows use the last DM (kernel clamp)
+            g = sh[idx].reshape(-1, tsy, self.NCH)
+            inc = int(np.diff(g, axis=1).max()) if tsy > 1 else 0
+            Dedispersion._spans[key] = (inc, int((g[:, -1, :] - g[:, 0, :]).max()))
+        return Dedispersion._spans[key]
+
+    def window_span(self, cfg: dict) -> int | None:
+        """SPAN of the register-window kernel (kernels/dedispersion.cu DD_WIN), or None.
+
+        Eligible: block_size_x == 32 (a warp's lanes share their DMs, so the
+        shifts are warp-uniform), strided samples (or one per lane),
+        contiguous DMs (or one per lane), adjacent DMs shifting by <= 1
+        sample, and a window of <= 4 samples.
+        """
+        if cfg["block_size_x"] != 32:
+            return None
+        if cfg["tile_size_x"] > 1 and cfg["tile_stride_x"] != 1:
+            return None
+        if cfg["tile_size_y"] > 1 and cfg["tile_stride_y"] != 0:
+            return None
+        inc, span = self._group_span(cfg["tile_size_y"])
+        if inc > 1 or span > 3:
+            return None
+        return span
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
@@ -530,7 +591,7 @@ class Dedispersion(Problem):
                 math.ceil(self.NSAMP / (cfg["block_size_x"] * cfg["tile_size_x"])), 1)
         return [Launch(kernel, grid, (cfg["block_size_x"], cfg["block_size_y"], 1),
                        [_u64(bufs["out"]), _u64(bufs["in"]), C.c_float(self.dm_first),
-                        C.c_float(self.dm_step)])]
+                        C.c_float(self.dm_step)], smem=self.smem_bytes(cfg))]
 
     def reference_launches(self, kernel, bufs: dict) -> list:
         from .runtime import Launch

@@ -190,3 +190,27 @@ def test_gemm_tc_tf32_within_k_scaled_tolerance(device):
         assert tgt.extras["256,4"]["verify"]["max_abs_err"] <= big.abs_tol
     finally:
         tgt.close()
+
+
+def test_dedispersion_window_mode_bit_exact(device):
+    """Register-window dedispersion (warp-uniform shifts, pattern dispatch,
+    FADD2): every eligible configuration of the space, bit-exact vs the C
+    oracle on a problem whose 8-DM groups span up to 3 samples."""
+    prob = Dedispersion(channels=96, samples=1500, dms=512, dm_step=0.07, ch_bw_mhz=1.0)
+    want = K.answer(prob)
+    names = prob.space.param_names
+    configs = [c for c in prob.space.enumerate_configs()
+               if prob.window_span(dict(zip(names, c))) is not None]
+    assert len(configs) >= 20
+    assert max(prob.window_span(dict(zip(names, c))) for c in configs) == 3
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        for c in configs:
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+            st, out = tgt.run_output(c)
+            assert st is Status.OK, (c, out)
+            diff = int(np.sum(out != want))
+            assert diff == 0, f"window {c}: {diff} elements differ"
+    finally:
+        tgt.close()
