@@ -51,7 +51,7 @@ WORKLOADS = {
                     desc="hotspot 4096x4096 fp32, 20 iterations, temporal_tiling_factor 1-10 sweep"),
     "convolution": dict(param="tile_size_y", batch=24,
                         desc="convolution 4096x4096 fp32, 15x15 filter"),
-    "dedispersion": dict(param="tile_size_y", batch=8,
+    "dedispersion": dict(param="block_size_x", batch=8,
                          desc="dedispersion 1536 ch x 2048 DM x 25000 samples fp32"),
     "gemm": dict(param="VWM", batch=12, desc="gemm 4096^3 fp32 CLBlast space"),
     "gemm_tc": dict(param=None, batch=8, desc="gemm 4096^3 tf32 tcgen05/TMEM/TMA variant (BN_T x STAGES)"),

@@ -27,6 +27,7 @@
 #ifndef REFERENCE_ONLY
 
 #define MWI (MWG / MDIMC)
+#define MP ((MWI + 1) / 2)
 #define NWI (NWG / NDIMC)
 #define KDIMA ((MDIMC * NDIMC) / MDIMA)
 #define KDIMB ((MDIMC * NDIMC) / NDIMB)
@@ -139,11 +140,14 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
   const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
   float rb[KWB][NWB / VWN][VWN];
 #endif
-  float acc[NWI][MWI];
+  // accumulators as M-pairs: the rank-1 update of a k step is packed FFMA2
+  // (a pair of A values x a broadcast B value), per component the same fmaf
+  // as the scalar form -> bit-identical; odd MWI keeps a scalar last row
+  float2 acc[NWI][MP];
 #pragma unroll
   for (int j = 0; j < NWI; ++j)
 #pragma unroll
-    for (int i = 0; i < MWI; ++i) acc[j][i] = 0.f;
+    for (int i = 0; i < MP; ++i) acc[j][i] = make_float2(0.f, 0.f);
 
   auto fetch = [&](int kw) {
 #if SA
@@ -223,7 +227,12 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
 #pragma unroll
       for (int j = 0; j < NWI; ++j)
 #pragma unroll
-        for (int i = 0; i < MWI; ++i) acc[j][i] = fmaf(a[i], b[j], acc[j][i]);
+        for (int i = 0; i < MP; ++i) {
+          if (2 * i + 1 < MWI)
+            acc[j][i] = __ffma2_rn(make_float2(a[2 * i], a[2 * i + 1]), make_float2(b[j], b[j]), acc[j][i]);
+          else
+            acc[j][i].x = fmaf(a[2 * i], b[j], acc[j][i].x);
+        }
     }
 #if SA || SB
     if (more) stage(buf ^ 1);
@@ -241,7 +250,13 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
 #pragma unroll
       for (int i = 0; i < MWI / VWM; ++i) {
         const int m = m0 + vidx_m(i, tx) * VWM;
-        stv<VWM>(C + (size_t)n * GM + m, &acc[j * VWN + w][i * VWM]);
+        float v[VWM];
+#pragma unroll
+        for (int u = 0; u < VWM; ++u) {
+          const int e = i * VWM + u;
+          v[u] = (e % 2 == 0) ? acc[j * VWN + w][e / 2].x : acc[j * VWN + w][e / 2].y;
+        }
+        stv<VWM>(C + (size_t)n * GM + m, v);
       }
     }
 }

@@ -139,6 +139,16 @@ def roofline(problem, cfg: dict, info: dict, peaks: dict) -> dict:
                 "peak_source": "0.5 x MEASURED_PEAKS bf16_tflops (tf32 = half-rate bf16)",
                 "alt": {"hbm_gbs": round(byts / t / 1e9, 2)}}
     fp32 = peaks.get("fp32_tflops", 0.0) * 1e12
+    if getattr(problem, "space_name", "") == "dedispersion":
+        # add-only kernel: the FP32 pipe retires one FADD per lane per cycle
+        # (FADD2 = two adds in two cycles), i.e. half the FFMA FLOP rate
+        tadd = 0.5 * fp32
+        ta = flop / t
+        return {"bound": "fp32", "achieved": round(ta / 1e12, 3), "peak": round(tadd / 1e12, 3),
+                "unit": "Tadd/s", "frac": round(ta / tadd, 4), "traffic": None,
+                "peak_source": "0.5 x in-run FFMA probe (FADD = 1 FLOP per FMA-pipe slot)",
+                "alt": {"paper_gbs": round(4.0 * flop / t / 1e9, 1),
+                        "hbm_gbs": round(byts / t / 1e9, 2)}}
     t_hbm = byts / hbm_peak
     t_fp = flop / fp32 if fp32 else 0.0
     gbs = byts / t / 1e9
