@@ -151,18 +151,13 @@ def cuda_run(config: tuple, width: int = 16384, height: int = 16384, iterations:
     smem = slab_prob.smem_bytes(cfg)
     if smem > 48 * 1024:
         kern.set_max_dynamic_smem(smem)
-    k = slab_prob.k
-    ow = cfg["block_size_x"] * cfg["tile_size_x"]
-    oh = cfg["block_size_y"] * cfg["tile_size_y"]
-    grid = (math.ceil(width / ow), math.ceil(slab.height / oh), 1)
+    if smem > 0:
+        kern.set_smem_carveout(100)
+    shape = slab_prob.launch_shape(cfg, kern)  # stream mode: segments sized to this slab
     torch.cuda.synchronize()
 
     def step(src, dst, nsteps):
-        launch = rt.Launch(kern, grid, (cfg["block_size_x"], cfg["block_size_y"], 1),
-                           [C.c_uint64(dst.data_ptr()), C.c_uint64(src.data_ptr()),
-                            C.c_uint64(dev_p.data_ptr()), C.c_int(nsteps), C.c_float(k["sdc"]),
-                            C.c_float(k["rx1"]), C.c_float(k["ry1"]), C.c_float(k["rz1"]),
-                            C.c_float(k["amb"])], smem=smem)
+        launch = slab_prob.launch(cfg, kern, dst.data_ptr(), src.data_ptr(), dev_p.data_ptr(), nsteps, shape)
         code, err = dev.run([launch])
         if code != rt.OK:
             raise RuntimeError(err)

@@ -404,28 +404,38 @@ class Hotspot(Problem):
             src = dst
         return seq
 
-    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
-        from .runtime import Launch
+    def launch_shape(self, cfg: dict, kernel) -> tuple:
+        """(grid, block, smem, extra args) of one launch of this configuration.
 
-        plan = self.step_plan(cfg["temporal_tiling_factor"])
+        Stream mode sizes its row segments from the kernel's occupancy
+        (driver query through ``kernel.occupancy``) so the grid is whole
+        waves; block-tile modes use the paper's ceil(problem / tile) grid.
+        """
+        block = (cfg["block_size_x"], cfg["block_size_y"], 1)
         geo = self.stream_geometry(cfg)
-        extra = []
         if geo is not None:
             occ = getattr(kernel, "occupancy", None)
-            if occ is not None:  # size the row segments in whole waves of the real residency
+            if occ is not None:
                 bps = occ(cfg["block_size_x"] * cfg["block_size_y"], geo["smem"])
                 geo = self.stream_geometry(cfg, blocks_per_sm=max(1, bps), n_sm=kernel.sm_count)
-            grid = (geo["blocks"], 1, 1)  # warp tiles, strip-fastest
-            extra = [C.c_int(geo["segh"]), C.c_int(geo["nsegs"])]
-        else:
-            ow = cfg["block_size_x"] * cfg["tile_size_x"]
-            oh = cfg["block_size_y"] * cfg["tile_size_y"]
-            grid = (math.ceil(self.W / ow), math.ceil(self.H / oh), 1)
-        block = (cfg["block_size_x"], cfg["block_size_y"], 1)
-        smem = self.smem_bytes(cfg)
-        return self._chain(kernel, bufs, len(plan), lambda i, s, d: Launch(
-            kernel, grid, block, [_u64(d), _u64(s), _u64(bufs["power"]), C.c_int(plan[i])]
-            + self._coeff_args() + extra, smem=smem))
+            return (geo["blocks"], 1, 1), block, geo["smem"], [C.c_int(geo["segh"]), C.c_int(geo["nsegs"])]
+        ow = cfg["block_size_x"] * cfg["tile_size_x"]
+        oh = cfg["block_size_y"] * cfg["tile_size_y"]
+        return (math.ceil(self.W / ow), math.ceil(self.H / oh), 1), block, self.smem_bytes(cfg), []
+
+    def launch(self, cfg: dict, kernel, dst: int, src: int, power: int, nsteps: int, shape=None):
+        """One launch advancing ``src`` by ``nsteps`` into ``dst`` (raw device addresses)."""
+        from .runtime import Launch
+
+        grid, block, smem, extra = shape or self.launch_shape(cfg, kernel)
+        return Launch(kernel, grid, block, [C.c_uint64(int(dst)), C.c_uint64(int(src)), C.c_uint64(int(power)),
+                                            C.c_int(nsteps)] + self._coeff_args() + extra, smem=smem)
+
+    def launches(self, cfg: dict, kernel, bufs: dict) -> list:
+        plan = self.step_plan(cfg["temporal_tiling_factor"])
+        shape = self.launch_shape(cfg, kernel)
+        return self._chain(kernel, bufs, len(plan), lambda i, s, d: self.launch(
+            cfg, kernel, d.ptr, s.ptr, bufs["power"].ptr, plan[i], shape))
 
     def reference_launches(self, kernel, bufs: dict) -> list:
         from .runtime import Launch

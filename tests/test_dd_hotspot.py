@@ -67,3 +67,14 @@ def test_slab_geometry():
     assert (s2.halo_top, s2.halo_bot, s2.row0) == (7, 0, 200)
     with pytest.raises(ValueError):
         make_slab(0, 3, 301, 7)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", [(16, 4, 4, 1, 4, 2, 1), (32, 2, 4, 1, 8, 1, 1), (32, 16, 3, 2, 6, 6, 1)])
+def test_cuda_run_single_rank_bit_exact(config):
+    """The slab driver with the tuned kernel (stream and block-tile modes) on
+    one GPU equals the naive reference chain bit-for-bit."""
+    from paper_2407_11488_b200.dd_hotspot import cuda_run
+
+    r = cuda_run(config, width=1024, height=768, iterations=20, repeats=1, verify=True)
+    assert r["bit_exact"] is True, r
