@@ -304,6 +304,7 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
   // E/W neighbours of every level's OLD centre row (level k-1 row a),
   // hoisted into one convergence block
   float wla[TT], era[TT];
+  float2 pprev[NP2];  // power row of the previous level's row a
 #pragma unroll
   for (int k = 1; k <= TT; ++k) {
     const int sC = ((2 * PH - k) % 4 + 4) % 4;
@@ -321,9 +322,17 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     // E/W of the fresh centre row a+1 (row b's centre)
     const float wlb = __shfl_up_sync(0xffffffffu, COL(f0, TSX - 1), 1);
     const float erb = __shfl_down_sync(0xffffffffu, f0[0].x, 1);
+    // power rows a and a+1; row a+1 is the previous level's row a (reuse)
     float2 pa[NP2], pb[NP2];
     hs_power(pa, S, a);
-    hs_power(pb, S, a + 1);
+    if (k == 1) {
+      hs_power(pb, S, a + 1);
+    } else {
+#pragma unroll
+      for (int q = 0; q < NP2; ++q) pb[q] = pprev[q];
+    }
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) pprev[q] = pa[q];
     float2 na[NP2], nb[NP2];
     hs_row_update<EDGE>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, EDGE && a == 0,
                         EDGE && a == GH - 1, S, kk, k2);
