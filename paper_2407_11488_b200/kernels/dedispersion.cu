@@ -150,8 +150,11 @@ __device__ __forceinline__ void dd_dispatch(DdWin& st, int idx, const float* p) 
 __device__ __forceinline__ unsigned dd_smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
-__device__ __forceinline__ void dd_mbar_init(unsigned long long* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(dd_smem_u32(b)) : "memory");
+__device__ __forceinline__ void dd_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void dd_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dd_smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void dd_mbar_expect(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(bytes)
@@ -172,13 +175,13 @@ __device__ __forceinline__ void dd_bulk(void* dst, const void* src, unsigned byt
 
 // warp 0: stage chunk t (channels t*CC ..) into `stage`
 __device__ __forceinline__ void dd_issue_chunk(const float* __restrict__ in, float* stage, unsigned long long* bar,
-                                               int t, int sb, float dmb, int lane) {
+                                               int t, int sb, float dmb, int lane, const float* sdelay) {
   const int ch = t * CC + lane;
   const int nvalid = NCH - t * CC < CC ? NCH - t * CC : CC;
   if (lane == 0) dd_mbar_expect(bar, (unsigned)(nvalid * ROWLEN * 4));
   __syncwarp();
   if (ch < NCH) {
-    const int shb = __float2int_rz(__fmul_rn(dmb, d_delay[ch]));
+    const int shb = __float2int_rz(__fmul_rn(dmb, sdelay[ch]));
     const int a = (sb + shb) & ~3;
     dd_bulk(stage + lane * ROWLEN, in + (size_t)ch * IN_PITCH + a, ROWLEN * 4, bar);
   }
@@ -188,9 +191,15 @@ extern "C" __global__ void __launch_bounds__(BSX * BSY)
 dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float dm_first,
                     float dm_step) {
   extern __shared__ __align__(128) float smem[];
+  // [stages][CC][ROWLEN] rows | full[NSTAGE] | empty[NSTAGE] | delay[NCH] | pattern->case[NPAT]
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NSTAGE * CC * ROWLEN);
-  unsigned char* pidx = reinterpret_cast<unsigned char*>(bars + NSTAGE);  // pattern -> dense case
+  unsigned long long* empty = bars + NSTAGE;
+  float* sdelay = reinterpret_cast<float*>(empty + NSTAGE);
+  unsigned char* pidx = reinterpret_cast<unsigned char*>(sdelay + NCH);
   for (int p = threadIdx.y * 32 + threadIdx.x; p < NPAT; p += BSX * BSY) pidx[p] = (unsigned char)dd_rank(p);
+  // per-channel delays in smem: the per-chunk lookups index them by lane
+  // (a __constant__ read with 32 different addresses serialises 32-fold)
+  for (int c = threadIdx.y * 32 + threadIdx.x; c < NCH; c += BSX * BSY) sdelay[c] = d_delay[c];
   const int lane = threadIdx.x;  // BSX == 32: one warp per DM group
   const int w = threadIdx.y;
   const int sb = (int)blockIdx.y * (32 * TSX);  // block's first sample
@@ -199,14 +208,17 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   const float dmb = __fadd_rn(dm_first, __fmul_rn((float)db0, dm_step));
   if (w == 0 && lane == 0) {
 #pragma unroll
-    for (int b = 0; b < NSTAGE; ++b) dd_mbar_init(bars + b);
+    for (int b = 0; b < NSTAGE; ++b) {
+      dd_mbar_init(bars + b, 1);       // full: the producer's arrive + TMA bytes
+      dd_mbar_init(empty + b, BSY);    // empty: one arrival per consumer warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int nchunks = (NCH + CC - 1) / CC;
   if (w == 0)
     for (int t = 0; t < NSTAGE && t < nchunks; ++t)
-      dd_issue_chunk(in, smem + t * CC * ROWLEN, bars + t, t, sb, dmb, lane);
+      dd_issue_chunk(in, smem + t * CC * ROWLEN, bars + t, t, sb, dmb, lane, sdelay);
   DdWin st;
 #pragma unroll
   for (int j = 0; j < TSY; ++j)
@@ -219,7 +231,7 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
     int mine = 0;
     {
       const int ch = t * CC + lane < NCH ? t * CC + lane : NCH - 1;
-      const float dl = d_delay[ch];
+      const float dl = sdelay[ch];
       // DM values recomputed per chunk (cheaper than 8 live registers);
       // clamped overshoot rows compute a valid DM and are never stored
       const int shb = __float2int_rz(__fmul_rn(dmb, dl));
@@ -243,9 +255,15 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       const int pk = __shfl_sync(0xffffffffu, mine, c);
       dd_dispatch(st, pk & 0xff, srow + (pk >> 8));
     }
-    __syncthreads();  // every warp is done with this stage
-    if (w == 0 && t + NSTAGE < nchunks)
-      dd_issue_chunk(in, smem + stg * CC * ROWLEN, bars + stg, t + NSTAGE, sb, dmb, lane);
+    // release the stage: one arrival per warp; the producer (warp 0) refills
+    // it once all warps have arrived -- the other warps run ahead on the
+    // stages already in flight instead of meeting at a block barrier
+    __syncwarp();
+    if (lane == 0) dd_mbar_arrive(empty + stg);
+    if (w == 0 && t + NSTAGE < nchunks) {
+      dd_mbar_wait(empty + stg, (t / NSTAGE) & 1);
+      dd_issue_chunk(in, smem + stg * CC * ROWLEN, bars + stg, t + NSTAGE, sb, dmb, lane, sdelay);
+    }
   }
   const int s0 = sb + lane;
 #pragma unroll

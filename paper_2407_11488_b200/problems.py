@@ -558,7 +558,7 @@ class Dedispersion(Problem):
             return 0
         rowlen = (32 * cfg["tile_size_x"] + self.block_span(cfg) + span + 4 + 3) & ~3
         npat = 1 << (cfg["tile_size_y"] - 1)
-        return 4 * self.DD_STAGES * self.DD_CC * rowlen + 8 * self.DD_STAGES + npat
+        return 4 * self.DD_STAGES * self.DD_CC * rowlen + 16 * self.DD_STAGES + 4 * self.NCH + npat
 
     _spans: dict = {}
 

@@ -192,11 +192,16 @@ def test_gemm_tc_tf32_within_k_scaled_tolerance(device):
         tgt.close()
 
 
-def test_dedispersion_window_mode_bit_exact(device):
-    """Register-window dedispersion (warp-uniform shifts, pattern dispatch,
-    FADD2): every eligible configuration of the space, bit-exact vs the C
-    oracle on a problem whose 8-DM groups span up to 3 samples."""
-    prob = Dedispersion(channels=96, samples=1500, dms=512, dm_step=0.07, ch_bw_mhz=1.0)
+@pytest.mark.parametrize("shape", [(96, 1500, 512, 0.07), (100, 1500, 300, 0.06)],
+                         ids=["chunked", "ragged"])
+def test_dedispersion_window_mode_bit_exact(device, shape):
+    """Register-window dedispersion (warp-uniform shifts, TMA-staged rows,
+    pattern dispatch, FADD2): every eligible configuration of the space,
+    bit-exact vs the C oracle on problems whose 8-DM groups span up to 3
+    samples -- one with whole 32-channel chunks and 256-DM blocks, one with
+    a channel tail chunk, a partial DM block and a ragged sample tail."""
+    ch, ns, nd, step = shape
+    prob = Dedispersion(channels=ch, samples=ns, dms=nd, dm_step=step, ch_bw_mhz=1.0)
     want = K.answer(prob)
     names = prob.space.param_names
     configs = [c for c in prob.space.enumerate_configs()
