@@ -389,7 +389,8 @@ def our_arm(args, dist: Dist):
             info = target.extras.get(config_key(c), {})
             rows.append({"config": list(c), "status": o.status.value, "time_ms": o.time_ms,
                          "regs": info.get("regs"), "smem": info.get("smem_bytes"),
-                         "launch_ms": info.get("launch_ms")})
+                         "launch_ms": info.get("launch_ms"),
+                         "host_s": {k: round(v, 6) for k, v in info.items() if k.startswith("t_")}})
         Path(args.dump).write_text(json.dumps({"workload": args.workload, "rows": rows}))
     all_best = dist.gather_obj(best)
     if dist.rank == 0:

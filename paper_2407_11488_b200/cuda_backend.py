@@ -199,9 +199,11 @@ class CudaTarget:
         info["compile_wait_s"] = time.perf_counter() - t0
         if not res.ok:
             return Observation(Status.COMPILE_FAILED, detail=(res.error or res.log)[-2000:])
+        t1 = time.perf_counter()
         rc, mod = self.dev.load(res.image)
         if rc != rt.OK:
             return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(mod))
+        info["t_load_s"] = time.perf_counter() - t1
         try:
             for sym, data in self.problem.constants().items():
                 if mod.set_constant(sym, data) != rt.OK:
@@ -216,6 +218,8 @@ class CudaTarget:
             info.update(kern.attrs())
             info["smem_bytes"] = smem
             launches = self.problem.launches(cfg, kern, self.bufs)
+            t2 = time.perf_counter()
+            info["t_setup_s"] = t2 - t1 - info["t_load_s"]
             if self.verify:
                 # poison the output so a kernel that skips elements fails
                 self.dev._check(self.dev.lib.tsg_memset32(self.dev.ctx, self.out.ptr,
@@ -225,6 +229,8 @@ class CudaTarget:
                                            protocol.timeout_ms)
             if rc != rt.OK:
                 return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(times))
+            t3 = time.perf_counter()
+            info["t_run_s"] = t3 - t2
             info["launch_ms"] = self.dev.last_launch_times(len(launches))
             info["n_launches"] = len(launches)
             if self.verify:
@@ -245,7 +251,10 @@ class CudaTarget:
                                 f"nonfinite={cmp['n_nonfinite']} bad={cmp['n_bad']}"),
                     )
         finally:
+            t4 = time.perf_counter()
             mod.unload()
+            info["t_unload_s"] = time.perf_counter() - t4
+            info["t_total_s"] = time.perf_counter() - t0
             self.extras[key] = info
         self.stats["executed"] += 1
         self.stats["gpu_ms"] += sum(times)
