@@ -150,6 +150,7 @@ struct HsStream {
   int csrc[NCH];     // global column of each chunk (clamped into the grid)
   unsigned omask;    // chunks that are useful output columns
   unsigned lmask, rmask;  // owned cells at gx == 0 / gx == GW-1
+  bool xl, xr;            // this lane's first / last column is grid column 0 / GW-1
 };
 
 // chunk c of this lane inside a shared row (chunk-major: lanes contiguous)
@@ -224,7 +225,14 @@ __device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, i
 // One cell-pair row update (HS_STEP on columns 2q, 2q+1; bit-exact):
 // C = centre row, N/S rows, wl/er = W of column 0 / E of column TSX-1
 // (from the neighbour lanes), P = power row.
-template <bool EDGE>
+// Edge modes E (warp-uniform, chosen per warp tile):
+//   E & 3 == 0: interior strip (no horizontal clamp)
+//   E & 3 == 1: strip holding grid column 0 / GW-1 at a LANE boundary: the
+//               clamp is applied once per level to the shuffled neighbour
+//               value (wl/er), not per cell
+//   E & 3 == 2: boundary inside a lane's columns: per-cell selects
+//   E & 4     : top/bottom row segment: N/S clamps at rows 0 / GH-1
+template <int E>
 __device__ __forceinline__ void hs_row_update(float2 (&nv)[NP2], const float2* N, const float2* Cc,
                                               const float2* Sr, float wl, float er, const float2 (&P)[NP2],
                                               bool top, bool bot, const HsStream& S, const HsCoef& kk,
@@ -241,9 +249,11 @@ __device__ __forceinline__ void hs_row_update(float2 (&nv)[NP2], const float2* N
     float e0 = (j + 1 < TSX) ? t.y : er;
     float w1 = t.x;
     float e1 = (j + 2 < TSX) ? COL(Cc, j + 2) : er;
-    if (EDGE) {
+    if (E & 4) {
       n = top ? t : n;
       s = bot ? t : s;
+    }
+    if ((E & 3) == 2) {
       w0 = (S.lmask >> j) & 1u ? t.x : w0;
       e0 = (S.rmask >> j) & 1u ? t.x : e0;
       w1 = (S.lmask >> (j + 1)) & 1u ? t.y : w1;
@@ -293,7 +303,7 @@ __device__ __forceinline__ void hs_store_row(const HsStream& S, int ro, const fl
 // two fresh rows the previous level just produced (they then replace the
 // dead slots of rows a-3, a-2).  Slots: row x at (x - ia) & 3, static for
 // PH = ((i - ia) / 2) & 1.
-template <int PH, bool EDGE, bool FULL>
+template <int PH, int E, bool FULL>
 __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT][4][NP2], int i,
                                                const HsCoef& kk, const HsK2& k2) {
   hs_stage_pair(S, i + NR - 2);  // keep NG-1 row pairs in flight
@@ -310,6 +320,10 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     const int sC = ((2 * PH - k) % 4 + 4) % 4;
     wla[k - 1] = __shfl_up_sync(0xffffffffu, COL(R[k - 1][sC], TSX - 1), 1);
     era[k - 1] = __shfl_down_sync(0xffffffffu, R[k - 1][sC][0].x, 1);
+    if ((E & 3) == 1) {  // grid column 0 / GW-1 sits at this lane's edge: clamp = own value
+      wla[k - 1] = S.xl ? R[k - 1][sC][0].x : wla[k - 1];
+      era[k - 1] = S.xr ? COL(R[k - 1][sC], TSX - 1) : era[k - 1];
+    }
   }
 #pragma unroll
   for (int k = 1; k <= TT; ++k) {
@@ -320,8 +334,12 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     const int s0 = ((2 * PH - k + 1) % 4 + 4) % 4;  // row a+1 (fresh f0)
     const int s1 = ((2 * PH - k + 2) % 4 + 4) % 4;  // row a+2 (fresh f1)
     // E/W of the fresh centre row a+1 (row b's centre)
-    const float wlb = __shfl_up_sync(0xffffffffu, COL(f0, TSX - 1), 1);
-    const float erb = __shfl_down_sync(0xffffffffu, f0[0].x, 1);
+    float wlb = __shfl_up_sync(0xffffffffu, COL(f0, TSX - 1), 1);
+    float erb = __shfl_down_sync(0xffffffffu, f0[0].x, 1);
+    if ((E & 3) == 1) {
+      wlb = S.xl ? f0[0].x : wlb;
+      erb = S.xr ? COL(f0, TSX - 1) : erb;
+    }
     // power rows a and a+1; row a+1 is the previous level's row a (reuse)
     float2 pa[NP2], pb[NP2];
     hs_power(pa, S, a);
@@ -334,9 +352,9 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
 #pragma unroll
     for (int q = 0; q < NP2; ++q) pprev[q] = pa[q];
     float2 na[NP2], nb[NP2];
-    hs_row_update<EDGE>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, EDGE && a == 0,
-                        EDGE && a == GH - 1, S, kk, k2);
-    hs_row_update<EDGE>(nb, R[k - 1][sC], f0, f1, wlb, erb, pb, EDGE && a + 1 == 0, EDGE && a + 1 == GH - 1, S,
+    hs_row_update<E>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, (E & 4) && a == 0,
+                        (E & 4) && a == GH - 1, S, kk, k2);
+    hs_row_update<E>(nb, R[k - 1][sC], f0, f1, wlb, erb, pb, (E & 4) && a + 1 == 0, (E & 4) && a + 1 == GH - 1, S,
                         kk, k2);
 #pragma unroll
     for (int q = 0; q < NP2; ++q) {
@@ -355,7 +373,7 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
 // ---- one row per iteration (loop_unroll_factor_t == 1) --------------------
 // Level k-1 keeps rows a-1, a in a 3-slot ring (row x at (x - ia) mod 3,
 // static for PH = (i - ia) mod 3); the fresh row a+1 arrives from level k-1.
-template <int PH, bool EDGE, bool FULL>
+template <int PH, int E, bool FULL>
 __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[TT][3][NP2], int i,
                                                 const HsCoef& kk, const HsK2& k2) {
   hs_stage_row(S, i + NR - 1);  // keep NR-1 rows in flight (one group per row)
@@ -369,6 +387,10 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
     const int sC = ((PH - k) % 3 + 3) % 3;
     wla[k - 1] = __shfl_up_sync(0xffffffffu, COL(R[k - 1][sC], TSX - 1), 1);
     era[k - 1] = __shfl_down_sync(0xffffffffu, R[k - 1][sC][0].x, 1);
+    if ((E & 3) == 1) {  // grid column 0 / GW-1 sits at this lane's edge: clamp = own value
+      wla[k - 1] = S.xl ? R[k - 1][sC][0].x : wla[k - 1];
+      era[k - 1] = S.xr ? COL(R[k - 1][sC], TSX - 1) : era[k - 1];
+    }
   }
 #pragma unroll
   for (int k = 1; k <= TT; ++k) {
@@ -380,8 +402,8 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
     float2 pa[NP2];
     hs_power(pa, S, a);
     float2 na[NP2];
-    hs_row_update<EDGE>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, EDGE && a == 0,
-                        EDGE && a == GH - 1, S, kk, k2);
+    hs_row_update<E>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, (E & 4) && a == 0,
+                        (E & 4) && a == GH - 1, S, kk, k2);
 #pragma unroll
     for (int q = 0; q < NP2; ++q) {
       R[k - 1][s0][q] = f0[q];
@@ -391,7 +413,7 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
   hs_store_row(S, i - (FULL ? TT : S.nsteps), f0);
 }
 
-template <bool EDGE, bool FULL>
+template <int E, bool FULL>
 __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& kk) {
   const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
                 make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
@@ -403,16 +425,16 @@ __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& 
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
   for (int i = S.ia; i <= S.ib; i += 3) {
-    hs_stream_iter1<0, EDGE, FULL>(S, R, i, kk, k2);
+    hs_stream_iter1<0, E, FULL>(S, R, i, kk, k2);
     if (i + 1 > S.ib) break;
-    hs_stream_iter1<1, EDGE, FULL>(S, R, i + 1, kk, k2);
+    hs_stream_iter1<1, E, FULL>(S, R, i + 1, kk, k2);
     if (i + 2 > S.ib) break;
-    hs_stream_iter1<2, EDGE, FULL>(S, R, i + 2, kk, k2);
+    hs_stream_iter1<2, E, FULL>(S, R, i + 2, kk, k2);
   }
 }
 
 // ---- two rows per iteration (loop_unroll_factor_t > 1) -----------------------
-template <bool EDGE, bool FULL>
+template <int E, bool FULL>
 __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
   const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
                 make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
@@ -424,16 +446,16 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
   for (int i = S.ia; i <= S.ib; i += 4) {
-    hs_stream_iter<0, EDGE, FULL>(S, R, i, kk, k2);
+    hs_stream_iter<0, E, FULL>(S, R, i, kk, k2);
     if (i + 2 > S.ib) break;
-    hs_stream_iter<1, EDGE, FULL>(S, R, i + 2, kk, k2);
+    hs_stream_iter<1, E, FULL>(S, R, i + 2, kk, k2);
   }
 }
 
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
                const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
-               float rz1, float amb, int segh, int nsegs) {
+               float rz1, float amb, int segh, int nsegs, int segh0) {
   extern __shared__ __align__(128) float smem[];
   const int tid = threadIdx.y * BSX + threadIdx.x;
   const int wid = tid >> 5;
@@ -449,11 +471,16 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   S.pring = S.tring + NR * SW;
   S.gx0 = strip * UW - TA;
   S.nsteps = nsteps;
-  S.y0 = seg * segh;
-  S.y1 = min(S.y0 + segh, GH);
+  // segments: the first (and, by the host's choice of segh, the last) are
+  // shorter -- their warps pay the N/S boundary selects, so all warps of the
+  // single wave finish together
+  S.y0 = seg == 0 ? 0 : segh0 + (seg - 1) * segh;
+  S.y1 = seg == nsegs - 1 ? GH : min(S.y0 + (seg == 0 ? segh0 : segh), GH);
   S.ia = max(0, S.y0 - nsteps);
   S.ib = S.y1 - 1 + nsteps;
   S.omask = S.lmask = S.rmask = 0u;
+  S.xl = S.gx0 + S.lane * TSX == 0;
+  S.xr = S.gx0 + S.lane * TSX + TSX - 1 == GW - 1;
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
     const int wc = S.lane * TSX + c * CW;  // window column of the chunk
@@ -478,24 +505,32 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   }
 #endif
   const HsCoef kk{sdc, rx1, ry1, rz1, amb};
-  const bool edge = S.gx0 <= 0 || S.gx0 + SW > GW - 1 || S.ia == 0 || S.ib >= GH - 1;
-  // the full-depth launches (nsteps == TT) run a static level loop; only the
-  // remainder launch of ceil(20/TT) takes the dynamic one
+  // edge mode of this warp tile (see hs_row_update)
+  const bool xedge = S.gx0 <= 0 || S.gx0 + SW > GW - 1;
+  const bool xalign = (S.gx0 > 0 || (-S.gx0) % TSX == 0) && (S.gx0 + SW <= GW - 1 || (GW - S.gx0) % TSX == 0);
+  const bool yedge = S.ia == 0 || S.ib >= GH - 1;
+  const int em = (xedge ? (xalign ? 1 : 2) : 0) | (yedge ? 4 : 0);
 #if HS_RPI == 2
 #define HS_RUN hs_stream_run
 #else
 #define HS_RUN hs_stream_run1
 #endif
+  // full-depth launches (nsteps == TT) run a static level loop; only the
+  // remainder launch of ceil(20/TT) takes the dynamic one (interior or
+  // all-selects edge variant)
   if (nsteps == TT) {
-    if (edge)
-      HS_RUN<true, true>(S, kk);
-    else
-      HS_RUN<false, true>(S, kk);
+    switch (em) {
+      case 0: HS_RUN<0, true>(S, kk); break;
+      case 1: HS_RUN<1, true>(S, kk); break;
+      case 4: HS_RUN<4, true>(S, kk); break;
+      case 5: HS_RUN<5, true>(S, kk); break;
+      default: HS_RUN<6, true>(S, kk); break;
+    }
   } else {
-    if (edge)
-      HS_RUN<true, false>(S, kk);
+    if (em == 0)
+      HS_RUN<0, false>(S, kk);
     else
-      HS_RUN<false, false>(S, kk);
+      HS_RUN<6, false>(S, kk);
   }
   cp_wait<0>();  // no copy may land in smem after the warp has left
 }

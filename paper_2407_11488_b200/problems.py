@@ -347,11 +347,35 @@ class Hotspot(Problem):
             by_smem = (228 * 1024) // (smem + 1024) if smem else 32
             blocks_per_sm = max(1, min(by_regs, by_smem, 32, 64 // wpb))
         wave = max(1, blocks_per_sm * wpb * n_sm // nstrips)  # row segments per strip, one wave
-        nsegs = min(tsy * wave, -(-self.H // 8))
-        segh = -(-self.H // nsegs)
-        nsegs = -(-self.H // segh)
-        return dict(sw=sw, ta=ta, uw=uw, segh=segh, wpb=wpb, smem=smem, nstrips=nstrips,
+        nsegs = max(1, min(tsy * wave, self.H // max(8, 2 * t)))
+        segh, segh0, nsegs = self._segments(nsegs)
+        return dict(sw=sw, ta=ta, uw=uw, segh=segh, segh0=segh0, wpb=wpb, smem=smem, nstrips=nstrips,
                     nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb), blocks_per_sm=blocks_per_sm)
+
+    # top/bottom segment height relative to the others (measured optimum on B200;
+    # TSG_HS_EDGE_SEG overrides it for experiments)
+    STREAM_EDGE_SEG = float(os.environ.get("TSG_HS_EDGE_SEG", "0.25"))
+
+    def _segments(self, nsegs: int) -> tuple:
+        """(segh, segh0, nsegs): interior and first segment heights, segment count.
+
+        The first and last segments are ~STREAM_EDGE_SEG of the others:
+        their warps pay the N/S boundary selects, and in a single wave the
+        slowest warp sets the launch time.  Rows: segh0 + (nsegs-2)*segh +
+        last = H with 0 < last <= segh.
+        """
+        if nsegs == 1:
+            return self.H, self.H, 1
+        f = self.STREAM_EDGE_SEG
+        segh = max(1, int(self.H // (nsegs - 2 + 2 * f)))
+        while self.H - (nsegs - 2) * segh > 2 * segh:  # edge segments must not exceed segh
+            segh += 1
+        rest = self.H - (nsegs - 2) * segh  # split over the first and last segment
+        segh0 = rest // 2
+        if segh0 < 1 or rest - segh0 < 1:  # too many segments for H: no edge shortening
+            segh = -(-self.H // nsegs)
+            return segh, segh, -(-self.H // segh)
+        return segh, segh0, nsegs
 
     def kernel_mode(self, cfg: dict) -> tuple:
         """(mode, floats per buffer, guard floats, buffers) -- mirrors kernels/hotspot.cu macros."""
@@ -418,7 +442,8 @@ class Hotspot(Problem):
             if occ is not None:
                 bps = occ(cfg["block_size_x"] * cfg["block_size_y"], geo["smem"])
                 geo = self.stream_geometry(cfg, blocks_per_sm=max(1, bps), n_sm=kernel.sm_count)
-            return (geo["blocks"], 1, 1), block, geo["smem"], [C.c_int(geo["segh"]), C.c_int(geo["nsegs"])]
+            return (geo["blocks"], 1, 1), block, geo["smem"], [C.c_int(geo["segh"]), C.c_int(geo["nsegs"]),
+                                                               C.c_int(geo["segh0"])]
         ow = cfg["block_size_x"] * cfg["tile_size_x"]
         oh = cfg["block_size_y"] * cfg["tile_size_y"]
         return (math.ceil(self.W / ow), math.ceil(self.H / oh), 1), block, self.smem_bytes(cfg), []

@@ -31,7 +31,8 @@ def test_stream_geometry_invariants():
         assert g["nstrips"] * g["uw"] >= prob.W and (g["nstrips"] - 1) * g["uw"] < prob.W
         assert g["nsegs"] * g["segh"] >= prob.H
         assert g["blocks"] * g["wpb"] >= g["nstrips"] * g["nsegs"]
-        assert g["segh"] * (g["nsegs"] - 1) < prob.H
+        last = prob.H - g["segh0"] - (g["nsegs"] - 2) * g["segh"] if g["nsegs"] > 1 else prob.H
+        assert 0 < g["segh0"] <= g["segh"] and 0 < last <= g["segh"]  # segments tile the rows
         assert (g["sw"] * 4) % 16 == 0  # bulk-copy row size
         assert g["smem"] <= Hotspot.STREAM_SMEM_MAX
         assert prob.smem_bytes(d) == g["smem"]
@@ -52,3 +53,18 @@ def test_stream_mode_needs_aligned_width():
 
 class _Fake:
     ptr = 0
+
+
+def test_stream_segments_tile_the_rows():
+    """Every segment count the launcher can ask for yields segments that tile
+    [0, H) exactly as the kernel computes them (first/last shortened)."""
+    for h in (Hotspot(), Hotspot(width=520, height=264), Hotspot(width=64, height=7)):
+        for n in range(1, min(h.H, 600) + 1):
+            segh, segh0, nsegs = h._segments(n)
+            prev = 0
+            for seg in range(nsegs):
+                y0 = 0 if seg == 0 else segh0 + (seg - 1) * segh
+                y1 = h.H if seg == nsegs - 1 else min(y0 + (segh0 if seg == 0 else segh), h.H)
+                assert y0 == prev and y1 > y0 and y1 - y0 <= segh, (h.H, n, seg)
+                prev = y1
+            assert prev == h.H
