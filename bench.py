@@ -286,7 +286,8 @@ def our_arm(args, dist: Dist):
     timed_sets = [step_configs(space, wl, batch, args.seed, args.warmup + s, dist.rank, dist.world)
                   for s in range(args.steps)]
     t0 = time.perf_counter()
-    futs = [compiler.submit(target.source, prob.options(dict(zip(space.param_names, c))))
+    futs = [compiler.submit(target.source_for(dict(zip(space.param_names, c))),
+                            prob.options(dict(zip(space.param_names, c))))
             for cs in timed_sets for c in cs]
     for f in futs:
         f.result()

@@ -168,6 +168,10 @@ class CudaTarget:
     def _options(self, cfg: dict) -> list:
         return self.problem.options(cfg)
 
+    def source_for(self, cfg: dict) -> str:
+        """Kernel source of one configuration (some problems generate code per config)."""
+        return self.problem.source_for(cfg, self.source)
+
     def prefetch(self, configs) -> None:
         """Queue compilation of upcoming configurations (bounded window)."""
         names = self.problem.space.param_names
@@ -177,12 +181,12 @@ class CudaTarget:
             key = config_key(config)
             if key not in self._pending:
                 cfg = dict(zip(names, config))
-                self._pending[key] = self.compiler.submit(self.source, self._options(cfg))
+                self._pending[key] = self.compiler.submit(self.source_for(cfg), self._options(cfg))
 
     def _compiled(self, key: str, cfg: dict) -> rt.CompileResult:
         fut = self._pending.pop(key, None)
         if fut is None:
-            fut = self.compiler.submit(self.source, self._options(cfg))
+            fut = self.compiler.submit(self.source_for(cfg), self._options(cfg))
         return fut.result()
 
     # -- the protocol ------------------------------------------------------------------

@@ -187,6 +187,11 @@ __device__ __forceinline__ void dd_issue_chunk(const float* __restrict__ in, flo
   }
 }
 
+// Even tile_size_x: the host splices in a generated inline-PTX dispatch here
+// (problems.dd_asm_dispatch: one case per pattern, brx.idx jump table); the
+// accumulators are then packed fp32x2 words updated by add.rn.f32x2.
+// @DD_ASM_DISPATCH@
+
 extern "C" __global__ void __launch_bounds__(BSX * BSY)
 dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float dm_first,
                     float dm_step) {
@@ -219,11 +224,19 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   if (w == 0)
     for (int t = 0; t < NSTAGE && t < nchunks; ++t)
       dd_issue_chunk(in, smem + t * CC * ROWLEN, bars + t, t, sb, dmb, lane, sdelay);
+#ifdef DD_HAVE_ASM
+  unsigned long long acc[TSY][XP];
+#pragma unroll
+  for (int j = 0; j < TSY; ++j)
+#pragma unroll
+    for (int q = 0; q < XP; ++q) acc[j][q] = 0ull;  // (+0.0f, +0.0f)
+#else
   DdWin st;
 #pragma unroll
   for (int j = 0; j < TSY; ++j)
 #pragma unroll
     for (int q = 0; q < XP; ++q) st.acc[j][q] = make_float2(0.f, 0.f);
+#endif
   for (int t = 0; t < nchunks; ++t) {
     const int stg = t % NSTAGE;
     // lane c: this warp's offset into channel t*CC+c's staged row and the
@@ -253,7 +266,11 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
 #pragma unroll 1
     for (int c = 0; c < nch; ++c, srow += ROWLEN) {
       const int pk = __shfl_sync(0xffffffffu, mine, c);
+#ifdef DD_HAVE_ASM
+      dd_asm_dispatch(acc, pk & 0xff, dd_smem_u32(srow + (pk >> 8)));
+#else
       dd_dispatch(st, pk & 0xff, srow + (pk >> 8));
+#endif
     }
     // release the stage: one arrival per warp; the producer (warp 0) refills
     // it once all warps have arrived -- the other warps run ahead on the
@@ -273,8 +290,13 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
 #pragma unroll
     for (int q = 0; q < XP; ++q) {
       const int sa = s0 + 64 * q, sbb = sa + 32;
-      if (sa < NSAMP) o[sa] = st.acc[j][q].x;
-      if (2 * q + 1 < TSX && sbb < NSAMP) o[sbb] = st.acc[j][q].y;
+#ifdef DD_HAVE_ASM
+      const float2 v = make_float2(__uint_as_float((unsigned)acc[j][q]), __uint_as_float((unsigned)(acc[j][q] >> 32)));
+#else
+      const float2 v = st.acc[j][q];
+#endif
+      if (sa < NSAMP) o[sa] = v.x;
+      if (2 * q + 1 < TSX && sbb < NSAMP) o[sbb] = v.y;
     }
   }
 }

@@ -84,6 +84,11 @@ class Problem:
     def source(self) -> str:
         return _src(self.source_file)
 
+    def source_for(self, cfg: dict | None, base: str | None = None) -> str:
+        """Source compiled for ``cfg``: the kernel file, plus any per-config
+        generated code (default: none)."""
+        return base if base is not None else self.source()
+
     def problem_defines(self) -> dict:
         return {}
 
@@ -488,6 +493,56 @@ class Hotspot(Problem):
 K_DM = 4148.808  # s MHz^2 pc^-1 cm^3
 
 
+def dd_asm_dispatch(tsx: int, tsy: int, span: int) -> str:
+    """Inline-PTX jump-table dispatch of the window dedispersion kernel.
+
+    One case per increment pattern P with popcount <= ``span``, in the same
+    dense order as the kernel's ``dd_rank`` (span-major, then value).  A
+    case loads the popc(P)+1 window samples of every owned sample pair from
+    the staged row (shared memory) and adds them to the TSY x TSX/2 packed
+    accumulators (``add.rn.f32x2``, per lane identical to the C++ cases);
+    ``brx.idx`` makes ptxas emit an indexed jump (BRX) instead of the
+    compare tree a C++ switch is lowered to.
+    """
+    assert tsx % 2 == 0
+    xp = tsx // 2
+    pats = sorted((p for p in range(1 << (tsy - 1)) if bin(p).count("1") <= span),
+                  key=lambda p: (bin(p).count("1"), p))
+    nacc = tsy * xp
+    idx_op, addr_op = nacc, nacc + 1
+    body = ["{", ".reg .f32 lo, hi;"]
+    body += [f".reg .b64 w{q}_{k};" for q in range(xp) for k in range(span + 1)]
+    body.append("ts_%=: .branchtargets " + ", ".join(f"L{i}_%=" for i in range(len(pats))) + ";")
+    body.append(f"brx.idx.uni %{idx_op}, ts_%=;")
+    for i, p in enumerate(pats):
+        body.append(f"L{i}_%=:")
+        ps = bin(p).count("1")
+        for q in range(xp):
+            for k in range(ps + 1):
+                body.append(f" ld.shared.f32 lo, [%{addr_op}+{4 * (64 * q + k)}];")
+                body.append(f" ld.shared.f32 hi, [%{addr_op}+{4 * (64 * q + 32 + k)}];")
+                body.append(f" mov.b64 w{q}_{k}, {{lo, hi}};")
+        for j in range(tsy):
+            g = bin(p & ((1 << j) - 1)).count("1")
+            for q in range(xp):
+                a = j * xp + q
+                body.append(f" add.rn.f32x2 %{a}, %{a}, w{q}_{g};")
+        if i != len(pats) - 1:
+            body.append(" bra.uni D_%=;")
+    body.append("D_%=:")
+    body.append("}")
+    asm = "\\n".join(body)  # C string escapes: one PTX statement per line
+    outs = ", ".join(f'"+l"(acc[{j}][{q}])' for j in range(tsy) for q in range(xp))
+    return (
+        "#define DD_HAVE_ASM 1\n"
+        "__device__ __forceinline__ void dd_asm_dispatch(unsigned long long (&acc)[TSY][XP], int idx, unsigned saddr) {\n"
+        # volatile keeps it ordered after the (volatile) mbarrier wait; no
+        # "memory" clobber, so the compiler may overlap the next channel's
+        # shuffle/decode with the adds
+        f'  asm volatile("{asm}" : {outs} : "r"(idx), "r"(saddr));\n'
+        "}\n")
+
+
 def dm_delay_table(nch: int, f_min_mhz: float, ch_bw_mhz: float, t_samp_s: float) -> np.ndarray:
     """Per-channel delay in samples per unit DM (fp32), channel 0 = lowest.
 
@@ -562,6 +617,29 @@ class Dedispersion(Problem):
         if span is not None:
             d.update(DD_WIN=1, SPAN=span, BLKSPAN=self.block_span(cfg))
         return d
+
+    DD_ASM_MARKER = "// @DD_ASM_DISPATCH@"
+
+    def source_for(self, cfg: dict | None, base: str | None = None) -> str:
+        """Window-mode configurations where it pays get a generated
+        jump-table dispatch (``dd_asm_dispatch``, kernels/dedispersion.cu)."""
+        src = base if base is not None else self.source()
+        if cfg is None:
+            return src
+        span = self.window_span(cfg)
+        if span is None or not self.use_asm_dispatch(cfg["tile_size_x"], cfg["tile_size_y"], span):
+            return src
+        return src.replace(self.DD_ASM_MARKER, dd_asm_dispatch(cfg["tile_size_x"], cfg["tile_size_y"], span))
+
+    @staticmethod
+    def use_asm_dispatch(tsx: int, tsy: int, span: int) -> bool:
+        """Jump table only where it pays (measured on B200): a deep compare
+        tree (>= 32 live patterns) AND >= 16 packed adds per case -- with
+        less work per case the indirect branch's bubble costs more than the
+        few compares it replaces (e.g. (2,8): 6.3 -> 8.1 ms, (4,8): 4.88 ->
+        4.70 ms)."""
+        npat = sum(1 for p in range(1 << (tsy - 1)) if bin(p).count("1") <= span)
+        return tsx % 2 == 0 and npat >= 32 and tsy * (tsx // 2) >= 16
 
     DD_STAGES = 3  # kernels/dedispersion.cu NSTAGE
     DD_CC = 32     # channels per stage

@@ -1,0 +1,53 @@
+"""Host-side logic of the window dedispersion kernel (no GPU).
+
+* eligibility / SPAN / BLKSPAN from the exact fp32 shift table;
+* the generated inline-PTX jump-table dispatch: one case per increment
+  pattern of popcount <= SPAN, in the kernel's dense (span-major) order,
+  compiling with NVRTC for sm_100a.
+"""
+
+import re
+
+import numpy as np
+import pytest
+
+from paper_2407_11488_b200 import runtime as rt
+from paper_2407_11488_b200.problems import Dedispersion, dd_asm_dispatch, dm_shifts
+
+
+def test_window_eligibility_and_spans():
+    p = Dedispersion()
+    names = p.space.param_names
+    elig = [c for c in p.space.enumerate_configs() if p.window_span(dict(zip(names, c))) is not None]
+    assert len(elig) == 32 and all(c[0] == 32 and c[1] == 32 for c in elig)
+    sh = dm_shifts(p.delay, p.NDM, p.dm_first, p.dm_step).astype(np.int64)
+    assert np.diff(sh, axis=0).max() == 1  # adjacent DMs shift by 0 or 1 sample
+    g = sh.reshape(-1, 8, p.NCH)
+    assert p.window_span(dict(zip(names, (32, 32, 4, 8, 1, 0)))) == int((g[:, -1] - g[:, 0]).max()) == 3
+    blk = p.block_span(dict(zip(names, (32, 32, 4, 8, 1, 0))))
+    assert blk == int((sh[255::256] - sh[0::256]).max())
+    # smem: 3 stages x 32 rows + barriers + delay table + pattern table, under the opt-in cap
+    assert p.smem_bytes(dict(zip(names, (32, 32, 4, 8, 1, 0)))) < 227 * 1024
+
+
+@pytest.mark.parametrize("tsx,tsy,span", [(2, 1, 0), (2, 4, 1), (4, 6, 2), (4, 8, 3), (2, 8, 3)])
+def test_asm_dispatch_cases(tsx, tsy, span):
+    code = dd_asm_dispatch(tsx, tsy, span)
+    pats = [q for q in range(1 << (tsy - 1)) if bin(q).count("1") <= span]
+    labels = re.findall(r"L(\d+)_%=:", code)
+    assert [int(x) for x in labels] == list(range(len(pats)))
+    # adds per case = TSY x TSX/2 packed accumulators
+    assert code.count("add.rn.f32x2") == len(pats) * tsy * (tsx // 2)
+
+
+def test_asm_dispatch_source_compiles_for_sm100a():
+    p = Dedispersion()
+    names = p.space.param_names
+    cfg = dict(zip(names, (32, 32, 4, 8, 1, 0)))
+    src = p.source_for(cfg)
+    assert "#define DD_HAVE_ASM" in src
+    res = rt.compile_source(src, p.options(cfg))
+    assert res.ok, res.error
+    assert "#define DD_HAVE_ASM" not in p.source_for(dict(zip(names, (32, 32, 2, 4, 1, 0))))
+    odd = dict(zip(names, (32, 32, 3, 8, 1, 0)))
+    assert "#define DD_HAVE_ASM" not in p.source_for(odd)  # odd TSX keeps the C++ switch

@@ -11,5 +11,5 @@ for w in convolution gemm gemm_tc; do
 done
 timeout 900 python bench.py --workload dedispersion --steps 2 --warmup 1 --batch 12 --no-cpu-baseline --no-e2e --dump gpurun_out/dump_dedispersion.json > gpurun_out/bench_dedispersion.json 2> gpurun_out/bench_dedispersion.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 1 --batch 20 --no-cpu-baseline --no-e2e > gpurun_out/bench_ncu.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:hotspot_kernel -s 2 -c 1 -o gpurun_out/prof_hs_best -f python tools/run_config.py hotspot 16,4,4,1,4,2,1 --runs 2 > gpurun_out/ncu_hs_best.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:hotspot_kernel -s 2 -c 1 -o gpurun_out/prof_hs_best -f python tools/run_config.py hotspot 32,4,4,1,5,5,1 --runs 2 > gpurun_out/ncu_hs_best.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:dedispersion_kernel -s 1 -c 1 -o gpurun_out/prof_dd_best -f python tools/run_config.py dedispersion 32,32,4,8,1,0 --runs 1 > gpurun_out/ncu_dd_best.log 2>&1
