@@ -186,6 +186,19 @@ def parse_args(argv=None):
     return ap.parse_args(argv)
 
 
+def traffic_of(workload: str, key: str) -> dict:
+    """roofline.traffic (bytes per dominant launch) from the committed ncu table."""
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        tab = json.loads(p.read_text()).get(workload, {})
+    except (OSError, ValueError):
+        return {"traffic": None}
+    if key in tab:
+        return {"traffic": tab[key]["dram_bytes"], "traffic_source": tab[key]["source"]}
+    return {"traffic": None, "traffic_note": "best configuration of this sample not ncu-captured; "
+            "captured configurations: profiles/traffic.json"}
+
+
 def metric_name():
     return "best-config GB/s or GFLOP/s per kernel vs B200 roofline; configs benchmarked/sec"
 
@@ -331,6 +344,14 @@ def our_arm(args, dist: Dist):
                 "gflops": round(prob.flops(cfg) / t / 1e9, 2),
                 "gbs_compulsory": round(prob.compulsory_bytes(cfg) / t / 1e9, 2),
                 "verify_rel_err": info.get("verify_rel_err")}
+    # ncu-measured DRAM traffic of the dominant launch, when this best
+    # configuration was captured (profiles/traffic.json, tools/traffic_table.py)
+    if roof and best_c is not None:
+        roof.update(traffic_of(args.workload, config_key(best_c)))
+    # sweep efficiency: device time spent in the timed kernels of
+    # every configuration ((1 warmup + 7 runs) x its mean) over the step time
+    kern_ms = sum(8.0 * o.time_ms for _, o in ok)
+    sweep_eff = round(kern_ms / elapsed_ms, 4) if elapsed_ms > 0 else None
     times = [o.time_ms for _, o in ok]
     impact = None
     if times:
@@ -411,7 +432,7 @@ def our_arm(args, dist: Dist):
                      "compile_workers": compiler.pool._max_workers,
                      "precompile_s": round(precompile_s, 3)},
             "best_config": best, "best_config_per_rank": all_best if dist.world > 1 else None,
-            "tuning_impact": impact, "roofline": roof,
+            "tuning_impact": impact, "roofline": roof, "sweep_efficiency": sweep_eff,
             "peaks": {"hbm_gbs": peaks["hbm_gbs"], "hbm_source": peaks["source"],
                       "fp32_tflops": round(peaks["fp32_tflops"], 3),
                       "ffma_tflops": round(peaks.get("ffma_tflops", 0.0), 3),

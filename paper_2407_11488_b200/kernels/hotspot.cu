@@ -303,7 +303,7 @@ __device__ __forceinline__ void hs_store_row(const HsStream& S, int ro, const fl
 // two fresh rows the previous level just produced (they then replace the
 // dead slots of rows a-3, a-2).  Slots: row x at (x - ia) & 3, static for
 // PH = ((i - ia) / 2) & 1.
-template <int PH, int E, bool FULL>
+template <int PH, int E, int NS>
 __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT][4][NP2], int i,
                                                const HsCoef& kk, const HsK2& k2) {
   hs_stage_pair(S, i + NR - 2);  // keep NG-1 row pairs in flight
@@ -327,7 +327,7 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
   }
 #pragma unroll
   for (int k = 1; k <= TT; ++k) {
-    if (!FULL && k > S.nsteps) break;  // FULL: nsteps == TT (static: no exit phis)
+    if (k > NS) break;  // static level count: no exit phis
     const int a = i - k;
     const int sN = ((2 * PH - k - 1) % 4 + 4) % 4;  // row a-1
     const int sC = ((2 * PH - k) % 4 + 4) % 4;      // row a
@@ -365,7 +365,7 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     }
   }
   // f0, f1 = level nsteps at rows i - nsteps, i + 1 - nsteps
-  const int ro = i - (FULL ? TT : S.nsteps);
+  const int ro = i - NS;
   hs_store_row(S, ro, f0);
   hs_store_row(S, ro + 1, f1);
 }
@@ -373,7 +373,7 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
 // ---- one row per iteration (loop_unroll_factor_t == 1) --------------------
 // Level k-1 keeps rows a-1, a in a 3-slot ring (row x at (x - ia) mod 3,
 // static for PH = (i - ia) mod 3); the fresh row a+1 arrives from level k-1.
-template <int PH, int E, bool FULL>
+template <int PH, int E, int NS>
 __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[TT][3][NP2], int i,
                                                 const HsCoef& kk, const HsK2& k2) {
   hs_stage_row(S, i + NR - 1);  // keep NR-1 rows in flight (one group per row)
@@ -394,7 +394,7 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
   }
 #pragma unroll
   for (int k = 1; k <= TT; ++k) {
-    if (!FULL && k > S.nsteps) break;
+    if (k > NS) break;
     const int a = i - k;
     const int sN = ((PH - k - 1) % 3 + 3) % 3;
     const int sC = ((PH - k) % 3 + 3) % 3;
@@ -410,10 +410,10 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
       f0[q] = na[q];
     }
   }
-  hs_store_row(S, i - (FULL ? TT : S.nsteps), f0);
+  hs_store_row(S, i - NS, f0);
 }
 
-template <int E, bool FULL>
+template <int E, int NS>
 __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& kk) {
   const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
                 make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
@@ -425,16 +425,16 @@ __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& 
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
   for (int i = S.ia; i <= S.ib; i += 3) {
-    hs_stream_iter1<0, E, FULL>(S, R, i, kk, k2);
+    hs_stream_iter1<0, E, NS>(S, R, i, kk, k2);
     if (i + 1 > S.ib) break;
-    hs_stream_iter1<1, E, FULL>(S, R, i + 1, kk, k2);
+    hs_stream_iter1<1, E, NS>(S, R, i + 1, kk, k2);
     if (i + 2 > S.ib) break;
-    hs_stream_iter1<2, E, FULL>(S, R, i + 2, kk, k2);
+    hs_stream_iter1<2, E, NS>(S, R, i + 2, kk, k2);
   }
 }
 
 // ---- two rows per iteration (loop_unroll_factor_t > 1) -----------------------
-template <int E, bool FULL>
+template <int E, int NS>
 __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
   const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
                 make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
@@ -446,16 +446,22 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
   for (int i = S.ia; i <= S.ib; i += 4) {
-    hs_stream_iter<0, E, FULL>(S, R, i, kk, k2);
+    hs_stream_iter<0, E, NS>(S, R, i, kk, k2);
     if (i + 2 > S.ib) break;
-    hs_stream_iter<1, E, FULL>(S, R, i + 2, kk, k2);
+    hs_stream_iter<1, E, NS>(S, R, i + 2, kk, k2);
   }
 }
 
-extern "C" __global__ void __launch_bounds__(NTHREADS)
-hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
-               const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
-               float rz1, float amb, int segh, int nsegs, int segh0) {
+// One launch advancing NS (static) levels.  The full-depth launches of a run
+// use hotspot_kernel (NS = TT); the remainder launch of ceil(20/TT) uses
+// hotspot_rem_kernel (NS = HS_REM), so no code path has a runtime level
+// count -- a dynamic-depth path needs ~1.6x the registers (exit phis) and,
+// being part of the same kernel, would cap every launch's occupancy.
+template <int NS>
+__device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const float* __restrict__ tin,
+                                               const float* __restrict__ power, float sdc, float rx1,
+                                               float ry1, float rz1, float amb, int segh, int nsegs,
+                                               int segh0) {
   extern __shared__ __align__(128) float smem[];
   const int tid = threadIdx.y * BSX + threadIdx.x;
   const int wid = tid >> 5;
@@ -470,14 +476,14 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   S.tring = smem + wid * WARP_FLOATS;
   S.pring = S.tring + NR * SW;
   S.gx0 = strip * UW - TA;
-  S.nsteps = nsteps;
+  S.nsteps = NS;
   // segments: the first (and, by the host's choice of segh, the last) are
   // shorter -- their warps pay the N/S boundary selects, so all warps of the
   // single wave finish together
   S.y0 = seg == 0 ? 0 : segh0 + (seg - 1) * segh;
   S.y1 = seg == nsegs - 1 ? GH : min(S.y0 + (seg == 0 ? segh0 : segh), GH);
-  S.ia = max(0, S.y0 - nsteps);
-  S.ib = S.y1 - 1 + nsteps;
+  S.ia = max(0, S.y0 - NS);
+  S.ib = S.y1 - 1 + NS;
   S.omask = S.lmask = S.rmask = 0u;
   S.xl = S.gx0 + S.lane * TSX == 0;
   S.xr = S.gx0 + S.lane * TSX + TSX - 1 == GW - 1;
@@ -515,25 +521,33 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
 #else
 #define HS_RUN hs_stream_run1
 #endif
-  // full-depth launches (nsteps == TT) run a static level loop; only the
-  // remainder launch of ceil(20/TT) takes the dynamic one (interior or
-  // all-selects edge variant)
-  if (nsteps == TT) {
-    switch (em) {
-      case 0: HS_RUN<0, true>(S, kk); break;
-      case 1: HS_RUN<1, true>(S, kk); break;
-      case 4: HS_RUN<4, true>(S, kk); break;
-      case 5: HS_RUN<5, true>(S, kk); break;
-      default: HS_RUN<6, true>(S, kk); break;
-    }
-  } else {
-    if (em == 0)
-      HS_RUN<0, false>(S, kk);
-    else
-      HS_RUN<6, false>(S, kk);
+  switch (em) {
+    case 0: HS_RUN<0, NS>(S, kk); break;
+    case 1: HS_RUN<1, NS>(S, kk); break;
+    case 4: HS_RUN<4, NS>(S, kk); break;
+    case 5: HS_RUN<5, NS>(S, kk); break;
+    default: HS_RUN<6, NS>(S, kk); break;
   }
   cp_wait<0>();  // no copy may land in smem after the warp has left
 }
+
+extern "C" __global__ void __launch_bounds__(NTHREADS)
+hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
+               const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
+               float rz1, float amb, int segh, int nsegs, int segh0) {
+  (void)nsteps;  // == TT
+  hs_stream_body<TT>(out, tin, power, sdc, rx1, ry1, rz1, amb, segh, nsegs, segh0);
+}
+
+#if defined(HS_REM) && HS_REM > 0
+extern "C" __global__ void __launch_bounds__(NTHREADS)
+hotspot_rem_kernel(float* __restrict__ out, const float* __restrict__ tin,
+                   const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
+                   float rz1, float amb, int segh, int nsegs, int segh0) {
+  (void)nsteps;  // == HS_REM
+  hs_stream_body<HS_REM>(out, tin, power, sdc, rx1, ry1, rz1, amb, segh, nsegs, segh0);
+}
+#endif
 
 #else  // !HS_STREAM
 

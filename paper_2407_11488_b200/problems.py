@@ -302,12 +302,13 @@ class Hotspot(Problem):
         return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
                     UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"],
-                    HS_STREAM=int(self.stream_geometry(cfg) is not None))
+                    HS_STREAM=int(self.stream_geometry(cfg) is not None),
+                    HS_REM=self.iterations % cfg["temporal_tiling_factor"])
 
     # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
     STREAM_NR = 8            # cp.async input ring depth (rows; pairs per group)
     STREAM_SMEM_MAX = 200 * 1024
-    STREAM_REG_BASE = 56     # addresses, masks, coefficients, temporaries
+    STREAM_REG_BASE = 48     # addresses, masks, coefficients, temporaries
 
     def stream_geometry(self, cfg: dict, blocks_per_sm: int | None = None,
                         n_sm: int = 148) -> dict | None:
@@ -328,9 +329,9 @@ class Hotspot(Problem):
         if self.W % 4 or nthreads % 32:
             return None
         budget = min(255, 65536 // nthreads)
-        regs = 3 * t * tsx + 4 * tsx + 2 * t + self.STREAM_REG_BASE
-        if cfg["loop_unroll_factor_t"] > 1:  # two rows per iteration: second chain's temporaries
-            regs += 4 * tsx + 8
+        # fitted to ptxas counts of the static-depth kernel (tools/hs_regs.py):
+        # ~3.5 registers per (level x column), odd TSX pays a scalar tail
+        regs = math.ceil(3.5 * t * tsx) + self.STREAM_REG_BASE + (12 * t if tsx % 2 else 0)
         if regs > budget:
             return None
         sw = 32 * tsx
@@ -454,12 +455,33 @@ class Hotspot(Problem):
         return (math.ceil(self.W / ow), math.ceil(self.H / oh), 1), block, self.smem_bytes(cfg), []
 
     def launch(self, cfg: dict, kernel, dst: int, src: int, power: int, nsteps: int, shape=None):
-        """One launch advancing ``src`` by ``nsteps`` into ``dst`` (raw device addresses)."""
+        """One launch advancing ``src`` by ``nsteps`` into ``dst`` (raw device addresses).
+
+        Stream mode: the remainder launch (nsteps = iterations % T) runs the
+        module's ``hotspot_rem_kernel`` (static level count HS_REM).
+        """
         from .runtime import Launch
 
         grid, block, smem, extra = shape or self.launch_shape(cfg, kernel)
+        if extra and nsteps != cfg["temporal_tiling_factor"]:
+            assert nsteps == self.iterations % cfg["temporal_tiling_factor"], nsteps
+            kernel = self._rem_kernel(kernel, smem)
         return Launch(kernel, grid, block, [C.c_uint64(int(dst)), C.c_uint64(int(src)), C.c_uint64(int(power)),
                                             C.c_int(nsteps)] + self._coeff_args() + extra, smem=smem)
+
+    @staticmethod
+    def _rem_kernel(kernel, smem: int):
+        if kernel is None:  # host-side planning (tests): no module
+            return None
+        rem = getattr(kernel, "_hs_rem", None)
+        if rem is None:
+            rem = kernel.module.function("hotspot_rem_kernel")
+            if smem > 48 * 1024:
+                rem.set_max_dynamic_smem(smem)
+            if smem > 0:
+                rem.set_smem_carveout(100)
+            kernel._hs_rem = rem
+        return rem
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         plan = self.step_plan(cfg["temporal_tiling_factor"])
