@@ -116,11 +116,30 @@ __device__ __forceinline__ constexpr int vidx_n(int i, int t) {
   return STRN ? i * NDIMC + t : t * (NWI / VWN) + i;
 }
 
-// Software pipeline (our B200 implementation choice, not a tunable): the
-// next k-tile is fetched from HBM into registers while the current one is
-// consumed from shared memory; the staged operands are double-buffered in
-// dynamic shared memory, so each k-tile costs one barrier and its global
-// load latency is hidden behind KWG x MWI x NWI FMAs.
+// Software pipeline (our B200 implementation choice, not a tunable): staged
+// k-tiles travel global -> shared by cp.async (LDGSTS) with exactly the
+// thread-to-element mapping and vector widths of the CLBlast load tunables
+// (MDIMA/NDIMB re-shape, VWM/VWN widths, STRM/STRN), into a GEMM_NS-deep
+// shared ring: GEMM_NS-1 k-tiles are in flight while one is consumed, no
+// registers hold the prefetch (the register round trip cost ~30 registers
+// per thread and capped the larger register tiles' occupancy), one barrier
+// per k-tile.
+#define GEMM_NS 3
+
+template <int V>
+__device__ __forceinline__ void cp_async_vec(float* dst, const float* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  if constexpr (V == 1) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+  } else if constexpr (V == 2) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+  } else {
+#pragma unroll
+    for (int q = 0; q < V; q += 4)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d + 16 * (q / 4)), "l"(src + q) : "memory");
+  }
+}
+
 extern "C" __global__ void __launch_bounds__(MDIMC * NDIMC)
 gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __restrict__ B) {
   const int tid = threadIdx.x;
@@ -131,14 +150,12 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
   float* smem = reinterpret_cast<float*>(gemm_smem4);
 #endif
 #if SA
-  float* alm = smem;  // [2][KWG][MWG]
+  float* alm = smem;  // [GEMM_NS][KWG][MWG]
   const int la0 = tid % MDIMA, la1 = tid / MDIMA;
-  float ra[KWA][MWA / VWM][VWM];
 #endif
 #if SB
-  float* blm = smem + (SA ? 2 * KWG * MWG : 0);  // [2][KWG][NWG]
+  float* blm = smem + (SA ? GEMM_NS * KWG * MWG : 0);  // [GEMM_NS][KWG][NWG]
   const int lb0 = tid % NDIMB, lb1 = tid / NDIMB;
-  float rb[KWB][NWB / VWN][VWN];
 #endif
   // accumulators as M-pairs: the rank-1 update of a k step is packed FFMA2
   // (a pair of A values x a broadcast B value), per component the same fmaf
@@ -149,59 +166,44 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
 #pragma unroll
     for (int i = 0; i < MP; ++i) acc[j][i] = make_float2(0.f, 0.f);
 
-  auto fetch = [&](int kw) {
+  // issue the async copies of k-tile `kw` into ring slot `buf`, then commit
+  auto fetch = [&](int kw, int buf) {
+    if (kw < GK) {
 #if SA
 #pragma unroll
-    for (int kia = 0; kia < KWA; ++kia)
+      for (int kia = 0; kia < KWA; ++kia)
 #pragma unroll
-      for (int mia = 0; mia < MWA / VWM; ++mia) {
-        const int mv = STRM ? mia * MDIMA + la0 : la0 * (MWA / VWM) + mia;
-        ldv_global<VWM>(ra[kia][mia], A + (size_t)(kw + kia * KDIMA + la1) * GM + m0 + mv * VWM);
-      }
+        for (int mia = 0; mia < MWA / VWM; ++mia) {
+          const int mv = STRM ? mia * MDIMA + la0 : la0 * (MWA / VWM) + mia;
+          cp_async_vec<VWM>(alm + buf * KWG * MWG + (kia * KDIMA + la1) * MWG + mv * VWM,
+                            A + (size_t)(kw + kia * KDIMA + la1) * GM + m0 + mv * VWM);
+        }
 #endif
 #if SB
 #pragma unroll
-    for (int kib = 0; kib < KWB; ++kib)
+      for (int kib = 0; kib < KWB; ++kib)
 #pragma unroll
-      for (int nib = 0; nib < NWB / VWN; ++nib) {
-        const int nv = STRN ? nib * NDIMB + lb0 : lb0 * (NWB / VWN) + nib;
-        ldv_global<VWN>(rb[kib][nib], B + (size_t)(kw + kib * KDIMB + lb1) * GN + n0 + nv * VWN);
-      }
+        for (int nib = 0; nib < NWB / VWN; ++nib) {
+          const int nv = STRN ? nib * NDIMB + lb0 : lb0 * (NWB / VWN) + nib;
+          cp_async_vec<VWN>(blm + buf * KWG * NWG + (kib * KDIMB + lb1) * NWG + nv * VWN,
+                            B + (size_t)(kw + kib * KDIMB + lb1) * GN + n0 + nv * VWN);
+        }
 #endif
-  };
-  auto stage = [&](int buf) {
-#if SA
-#pragma unroll
-    for (int kia = 0; kia < KWA; ++kia)
-#pragma unroll
-      for (int mia = 0; mia < MWA / VWM; ++mia) {
-        const int mv = STRM ? mia * MDIMA + la0 : la0 * (MWA / VWM) + mia;
-        stv<VWM>(alm + buf * KWG * MWG + (kia * KDIMA + la1) * MWG + mv * VWM, ra[kia][mia]);
-      }
-#endif
-#if SB
-#pragma unroll
-    for (int kib = 0; kib < KWB; ++kib)
-#pragma unroll
-      for (int nib = 0; nib < NWB / VWN; ++nib) {
-        const int nv = STRN ? nib * NDIMB + lb0 : lb0 * (NWB / VWN) + nib;
-        stv<VWN>(blm + buf * KWG * NWG + (kib * KDIMB + lb1) * NWG + nv * VWN, rb[kib][nib]);
-      }
-#endif
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");  // (empty groups keep the count uniform)
   };
   (void)fetch;
-  (void)stage;
 
 #if SA || SB
-  fetch(0);
-  stage(0);
-  __syncthreads();
+#pragma unroll
+  for (int s = 0; s < GEMM_NS - 1; ++s) fetch(s * KWG, s);
 #endif
   int buf = 0;
   for (int kw = 0; kw < GK; kw += KWG) {
 #if SA || SB
-    const bool more = kw + KWG < GK;
-    if (more) fetch(kw + KWG);  // in flight during the FMAs below
+    asm volatile("cp.async.wait_group %0;" ::"n"(GEMM_NS - 2) : "memory");
+    __syncthreads();  // k-tile kw visible to all; everyone is done with the slot refilled below
+    fetch(kw + (GEMM_NS - 1) * KWG, (buf + GEMM_NS - 1) % GEMM_NS);
 #endif
 #pragma unroll
     for (int k = 0; k < KWG; ++k) {
@@ -235,9 +237,7 @@ gemm_kernel(float* __restrict__ C, const float* __restrict__ A, const float* __r
         }
     }
 #if SA || SB
-    if (more) stage(buf ^ 1);
-    __syncthreads();
-    buf ^= 1;
+    buf = (buf + 1) % GEMM_NS;
 #endif
   }
   (void)buf;

@@ -799,8 +799,10 @@ class Gemm(Problem):
         return dict(GM=self.M, GN=self.N, GK=self.K)
 
     def smem_bytes(self, cfg: dict) -> int:
-        # double-buffered staged k-tiles (kernels/gemm.cu)
-        return 4 * 2 * cfg["KWG"] * (cfg["MWG"] * cfg["SA"] + cfg["NWG"] * cfg["SB"])
+        # GEMM_NS-deep cp.async ring of staged k-tiles (kernels/gemm.cu)
+        return 4 * self.GEMM_NS * cfg["KWG"] * (cfg["MWG"] * cfg["SA"] + cfg["NWG"] * cfg["SB"])
+
+    GEMM_NS = 3
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
