@@ -145,7 +145,7 @@ __device__ __forceinline__ void dd_dispatch(DdWin& st, int idx, const float* p) 
 // load costs ~2.4 L1 wavefronts and an LSU queue slot).
 #define CC 32
 #define ROWLEN ((32 * TSX + BLKSPAN + SPAN + 4 + 3) & ~3)
-#define NSTAGE 3
+#define NSTAGE 5
 
 __device__ __forceinline__ unsigned dd_smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -201,7 +201,18 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   unsigned long long* empty = bars + NSTAGE;
   float* sdelay = reinterpret_cast<float*>(empty + NSTAGE);
   unsigned char* pidx = reinterpret_cast<unsigned char*>(sdelay + NCH);
-  for (int p = threadIdx.y * 32 + threadIdx.x; p < NPAT; p += BSX * BSY) pidx[p] = (unsigned char)dd_rank(p);
+  // pattern -> dense case index (span-major, then value): a counting loop
+  // (the constexpr dd_rank is recursive -- fine at compile time, a deep
+  // call chain at run time)
+  for (int p = threadIdx.y * 32 + threadIdx.x; p < NPAT; p += BSX * BSY) {
+    const int sp = __popc(p);
+    int r = 0;
+    for (int q = 0; q < NPAT; ++q) {
+      const int sq = __popc(q);
+      r += (sq <= SPAN) && (sq < sp || (sq == sp && q < p));
+    }
+    pidx[p] = (unsigned char)r;
+  }
   // per-channel delays in smem: the per-chunk lookups index them by lane
   // (a __constant__ read with 32 different addresses serialises 32-fold)
   for (int c = threadIdx.y * 32 + threadIdx.x; c < NCH; c += BSX * BSY) sdelay[c] = d_delay[c];

@@ -663,7 +663,7 @@ class Dedispersion(Problem):
         npat = sum(1 for p in range(1 << (tsy - 1)) if bin(p).count("1") <= span)
         return tsx % 2 == 0 and npat >= 32 and tsy * (tsx // 2) >= 16
 
-    DD_STAGES = 3  # kernels/dedispersion.cu NSTAGE
+    DD_STAGES = 5  # kernels/dedispersion.cu NSTAGE
     DD_CC = 32     # channels per stage
 
     def block_span(self, cfg: dict) -> int:
