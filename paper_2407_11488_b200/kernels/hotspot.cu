@@ -98,10 +98,13 @@ struct HsCoef {
 #define WPB (NTHREADS / 32)
 // input ring: NR rows = NG groups of 2 rows (one group per iteration),
 // NG-1 groups in flight
-#define NR 8
+#ifndef HS_NR
+#define HS_NR 8
+#endif
+#define NR HS_NR
 #define NG (NR / 2)
 // power ring: a power of two >= TT + NR + 2 rows (slot = row & (PR - 1))
-#define PR (SH_POWER ? ((TT + NR + 2) <= 16 ? 16 : 32) : 0)
+#define PR (SH_POWER ? ((TT + NR + 2) <= 16 ? 16 : ((TT + NR + 2) <= 32 ? 32 : 64)) : 0)
 #define WARP_FLOATS (SW * (NR + PR))
 // staging chunk (floats) and chunks per lane
 #define CW ((TSX % 4) == 0 ? 4 : ((TSX % 2) == 0 ? 2 : 1))

@@ -303,10 +303,18 @@ class Hotspot(Problem):
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
                     UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"],
                     HS_STREAM=int(self.stream_geometry(cfg) is not None),
-                    HS_REM=self.iterations % cfg["temporal_tiling_factor"])
+                    HS_REM=self.iterations % cfg["temporal_tiling_factor"], HS_NR=self.stream_nr(cfg["temporal_tiling_factor"]))
 
     # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
-    STREAM_NR = 8            # cp.async input ring depth (rows; pairs per group)
+    # cp.async input ring depth (rows): deeper for T >= 6 (measured on B200:
+    # T=8 0.238 -> 0.205 ms with 16 rows; T <= 5 unchanged or slightly slower);
+    # TSG_HS_NR forces one value for experiments
+    STREAM_NR_ENV = os.environ.get("TSG_HS_NR")
+
+    def stream_nr(self, t: int) -> int:
+        if self.STREAM_NR_ENV:
+            return int(self.STREAM_NR_ENV)
+        return 16 if t >= 6 else 8
     STREAM_SMEM_MAX = 200 * 1024
     STREAM_REG_BASE = 48     # addresses, masks, coefficients, temporaries
 
@@ -339,8 +347,8 @@ class Hotspot(Problem):
         uw = ((sw - ta - t) // 4) * 4
         if uw < 4:
             return None
-        nr = self.STREAM_NR
-        pr = (16 if t + nr + 2 <= 16 else 32) if shp else 0
+        nr = self.stream_nr(t)
+        pr = (16 if t + nr + 2 <= 16 else (32 if t + nr + 2 <= 32 else 64)) if shp else 0
         wpb = nthreads // 32
         warp_floats = sw * (nr + pr)
         smem = 4 * wpb * warp_floats
