@@ -117,54 +117,118 @@ class Dist:
 
 
 class ClockSampler:
+    """SM clocks + throttle reasons sampled during the timed region.
+
+    In-process NVML (pynvml), SM clock and clocks-event reasons only, taken
+    SYNCHRONOUSLY by the bench loop between configurations (``sample``):
+    any asynchronous poller -- ``nvidia-smi -lms`` (the fallback) or an NVML
+    thread -- contends with the driver and stalled concurrent module
+    load/unload calls by up to ~0.5 s (measured; none without a poller).
+    """
+
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    REASON_BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20,
+                   "hw_thermal_slowdown": 0x40}
 
-    def __init__(self, index: int):
+    def __init__(self, index: int, period_ms: int = 250):
         self.index = index
+        self.period_ms = period_ms
         self.proc = None
-        self.lines: list = []
+        self.kind = None
+        self.lines: list = []     # nvidia-smi fallback: (t, csv line)
+        self.samples: list = []   # nvml: (t, sm_mhz, reasons bitmask)
+        self.window = None        # (t0, t1) of the timed region (perf_counter)
+        self._stop = threading.Event()
 
     def start(self):
+        if os.environ.get("TSG_NO_CLOCK_SAMPLER"):  # diagnostics only: no clocks in the line
+            return
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM))
+            get = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None)
+            self._reasons = get or pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self.kind = "nvml"
+            self.sample()
+            return
+        except Exception:  # noqa: BLE001 -- fall back to nvidia-smi
+            self.kind = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                 "-i", str(self.index), "-lms", str(self.period_ms)], stdout=subprocess.PIPE,
                 stderr=subprocess.DEVNULL, text=True)
+            self.kind = "nvidia-smi"
             threading.Thread(target=self._pump, daemon=True).start()
         except OSError:
             self.proc = None
 
+    def sample(self) -> None:
+        """One synchronous NVML sample (called between configurations)."""
+        if self.kind != "nvml" or os.environ.get("TSG_NVML_NO_SAMPLES"):
+            return
+        try:
+            nv, h = self._nvml, self._h
+            self.samples.append((time.perf_counter(), float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                 int(self._reasons(h))))
+        except Exception:  # noqa: BLE001
+            pass
+
     def _pump(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
+
+    def mark(self, begin: bool) -> None:
+        """Bracket the timed region: only samples inside it are summarised."""
+        t = time.perf_counter()
+        self.window = (t, None) if begin else (self.window[0] if self.window else 0.0, t)
+
+    def _in_window(self, ts: float) -> bool:
+        lo, hi = self.window if self.window else (0.0, None)
+        return not (ts < lo - 0.3 or (hi is not None and ts > hi + 0.3))
 
     def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.15)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
+        if self.kind is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["clock sampler unavailable"]}
+        time.sleep(0.05)
+        self._stop.set()
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
+        if self.kind == "nvml":
+            for ts, mhz, bits in list(self.samples):
+                if self._in_window(ts):
+                    sm.append(mhz)
+                    reasons.update(n for n, b in self.REASON_BITS.items() if bits & b)
+            mx = [self.max_mhz]
+        else:
+            self.proc.terminate()
             try:
-                sm.append(float(parts[0]))
-                mx.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[3:7]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for ts, ln in self.lines:
+                if not self._in_window(ts):
+                    continue
+                parts = [p.strip() for p in ln.split(",")]
+                if len(parts) < 7:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    mx.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, parts[3:7]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.kind}
 
 
 # ----------------------------------------------------------------------------
@@ -270,6 +334,7 @@ def our_arm(args, dist: Dist):
     prob = make_problem(args.workload)
     t_setup = time.perf_counter()
     target = CudaTarget(prob, device=dev, compiler=compiler)
+    target.retire_cap = 1 << 14  # no batch unload inside any timed region (flushed at close)
     setup_s = time.perf_counter() - t_setup
     proto = MeasurementProtocol(warmup_runs=1, benchmark_runs=7, flush_l2=True)
     peaks = measured_peaks()
@@ -281,8 +346,16 @@ def our_arm(args, dist: Dist):
         for i, c in enumerate(configs):
             if i % 4 == 0:
                 target.prefetch(configs[i:])
+                sampler.sample()  # clocks/throttle reasons, between configurations
             obs.append((c, target.execute(c, proto)))
         return obs
+
+    # nvidia-smi is started here, BEFORE the warm-up: its NVML start-up holds
+    # driver locks for ~0.3 s and would otherwise stall the first timed
+    # configuration's module load/unload; samples are filtered to the timed
+    # region (mark) below
+    sampler = ClockSampler(dist.local)
+    sampler.start()
 
     # -- warmup steps double as the COLD measurement (NVRTC pipelined) -------
     cold_cfg, cold_s = 0, 0.0
@@ -308,17 +381,17 @@ def our_arm(args, dist: Dist):
 
     # -- timed region -----------------------------------------------------------
     launches0 = dev.launch_count
-    sampler = ClockSampler(dist.local)
     results = []
     dist.barrier()
     dev.mark(0)
-    sampler.start()
+    sampler.mark(True)
     t_wall = time.perf_counter()
     for cs in timed_sets:
         results.extend(run_step(cs))
     dev.mark(1)
     elapsed_ms = dev.elapsed_ms(0, 1)
     wall_s = time.perf_counter() - t_wall
+    sampler.mark(False)
     clocks = sampler.stop()
     dist.barrier()
     launches = dev.launch_count - launches0
@@ -327,6 +400,7 @@ def our_arm(args, dist: Dist):
     total = dist.sum(n_cfg)
     value = total / (t_max / 1000.0)
 
+    target.collect_attrs()  # registers etc. of the measured modules (untimed)
     ok = [(c, o) for c, o in results if o.ok]
     fails = {}
     for _, o in results:

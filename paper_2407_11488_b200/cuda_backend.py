@@ -129,6 +129,12 @@ class CudaTarget:
             else:
                 self._compute_answer()
         self.extras: dict = {}
+        # modules of measured configurations are unloaded in batches (flush_
+        # modules / close), not inside the per-configuration protocol: a
+        # cuModuleUnload of a large module occasionally blocks ~0.1-0.6 s in
+        # the driver (measured on B200), which would land inside a sweep
+        self._retired: list = []
+        self.retire_cap = 256
         self._pending: "OrderedDict[str, Future]" = OrderedDict()
         self.prefetch_depth = prefetch_depth or 4 * self.compiler.pool._max_workers
         self.stats = {"executed": 0, "gpu_ms": 0.0, "verify_failed": 0}
@@ -219,7 +225,8 @@ class CudaTarget:
                     return Observation(Status.INVALID, detail=rt.last_error())
             if smem > 0:
                 kern.set_smem_carveout(100)  # occupancy limited by smem use, not a default carveout
-            info.update(kern.attrs())
+            # register/static-smem attributes are read in batch when the module
+            # is retired (flush_modules): fewer driver calls per configuration
             info["smem_bytes"] = smem
             launches = self.problem.launches(cfg, kern, self.bufs)
             t2 = time.perf_counter()
@@ -256,7 +263,7 @@ class CudaTarget:
                     )
         finally:
             t4 = time.perf_counter()
-            mod.unload()
+            self._retire(mod, key, self.problem.kernel_name)
             info["t_unload_s"] = time.perf_counter() - t4
             info["t_total_s"] = time.perf_counter() - t0
             self.extras[key] = info
@@ -291,7 +298,29 @@ class CudaTarget:
         finally:
             mod.unload()
 
+    def _retire(self, mod, key: str | None = None, kernel_name: str | None = None) -> None:
+        self._retired.append((mod, key, kernel_name))
+        if len(self._retired) >= self.retire_cap:
+            self.flush_modules()
+
+    def collect_attrs(self) -> None:
+        """Fill ``extras[key]`` with register/smem attributes of retired modules."""
+        for mod, key, name in self._retired:
+            if key is not None and name and "regs" not in self.extras.get(key, {}):
+                try:
+                    self.extras.setdefault(key, {}).update(mod.function(name).attrs())
+                except Exception:  # noqa: BLE001 -- attributes are diagnostics
+                    pass
+
+    def flush_modules(self) -> None:
+        """Unload the modules of already-measured configurations."""
+        self.collect_attrs()
+        for mod, _, _ in self._retired:
+            mod.unload()
+        self._retired.clear()
+
     def close(self):
+        self.flush_modules()
         for b in self.bufs.values():
             b.free()
         if self.answer_buf:

@@ -102,6 +102,12 @@ _lib = None
 _lib_lock = threading.Lock()
 
 
+# Modules are loaded eagerly (all kernels at cuModuleLoadData) unless the user
+# chose otherwise: the tuning loop then pays the code upload in one predictable
+# call instead of inside the first function lookup / launch.
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
+
+
 def load_library(path: Path | str | None = None):
     """Load libtsgpu.so (raises DeviceError when it is absent)."""
     global _lib
