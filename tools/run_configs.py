@@ -35,6 +35,7 @@ for i, c in enumerate(cfgs):
     if i % 8 == 0:
         tgt.prefetch(cfgs[i:])
     obs = tgt.execute(c, proto)
+    tgt.collect_attrs()
     info = tgt.extras.get(config_key(c), {})
     mode = prob.kernel_mode(dict(zip(prob.space.param_names, c)))[0] if hasattr(prob, "kernel_mode") else None
     print(json.dumps({"config": list(c), "status": obs.status.value, "time_ms": obs.time_ms, "mode": mode,
