@@ -1,0 +1,52 @@
+"""Caches produced on the B200 by a full brute-force sweep (tools/full_sweep.py).
+
+The committed convolution cache covers all 4,362 valid configurations of the
+reference space, measured with the in-process ``cuda`` backend.  It must read
+back through our own reader and -- the parity bridge of SURVEY §8c -- import
+into the UNMODIFIED reference with ``expected_space`` (no SpaceMismatch) and
+yield a complete landscape (the reference's ``build_ffg`` raises
+IncompleteCache otherwise).
+"""
+
+import gzip
+import json
+from pathlib import Path
+
+import pytest
+
+from paper_2407_11488_b200.paramspace import bundled_space, config_key
+from paper_2407_11488_b200.store import import_external_cache, loads_cache
+
+CACHES = Path(__file__).resolve().parents[1] / "profiles" / "round1" / "caches"
+
+
+def _unzip(name: str, tmp_path: Path) -> Path:
+    p = tmp_path / name
+    p.write_bytes(gzip.decompress((CACHES / (name + ".gz")).read_bytes()))
+    return p
+
+
+def test_gpu_convolution_cache_is_complete(tmp_path):
+    space = bundled_space("convolution")
+    keys = {config_key(c) for c in space.enumerate_configs()}
+    native = loads_cache(_unzip("convolution.tunescape.json", tmp_path).read_text())
+    assert set(native.records) == keys and len(keys) == 4362
+    assert all(o.ok and o.time_ms > 0 and len(o.times_ms) == 7 for o in native.records.values())
+    kt = import_external_cache(_unzip("convolution.kerneltuner.json", tmp_path), expected_space=space)
+    assert set(kt.records) == keys
+    summary = json.loads((CACHES / "convolution.summary.json").read_text())
+    best = min(native.records.items(), key=lambda kv: kv[1].time_ms)
+    assert best[0] == ",".join(map(str, summary["best"]))
+
+
+def test_gpu_convolution_cache_imports_into_reference(tmp_path, reference_pkg):
+    from tunescape.landscape import build_ffg
+    from tunescape.paramspace import bundled_space as ref_space
+    from tunescape.store import import_external_cache as ref_import
+
+    rs = ref_space("convolution")
+    ref = ref_import(_unzip("convolution.kerneltuner.json", tmp_path), expected_space=rs)
+    assert len(ref.records) == 4362
+    assert ref.space_fingerprint == bundled_space("convolution").fingerprint()
+    ffg = build_ffg(ref, rs)  # raises IncompleteCache unless every valid configuration is present
+    assert ffg is not None
