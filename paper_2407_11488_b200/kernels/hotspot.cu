@@ -524,12 +524,25 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
 #else
 #define HS_RUN hs_stream_run1
 #endif
-  switch (em) {
-    case 0: HS_RUN<0, NS>(S, kk); break;
-    case 1: HS_RUN<1, NS>(S, kk); break;
-    case 4: HS_RUN<4, NS>(S, kk); break;
-    case 5: HS_RUN<5, NS>(S, kk); break;
-    default: HS_RUN<6, NS>(S, kk); break;
+  // instantiated edge modes (each one is a full copy of the stream loop, so
+  // they cost NVRTC time): the full-depth kernel keeps interior, lane-aligned
+  // X edge, X+Y edge (also taken by Y-only tiles: its wl/er selects are two
+  // per level) and the all-selects fallback; the single short remainder
+  // launch keeps interior, lane-aligned X edge and the fallback
+  if (NS == TT) {
+    switch (em) {
+      case 0: HS_RUN<0, NS>(S, kk); break;
+      case 1: HS_RUN<1, NS>(S, kk); break;
+      case 4:
+      case 5: HS_RUN<5, NS>(S, kk); break;
+      default: HS_RUN<6, NS>(S, kk); break;
+    }
+  } else {
+    switch (em) {  // Y-edge segments are short (STREAM_EDGE_SEG): the fallback absorbs them
+      case 0: HS_RUN<0, NS>(S, kk); break;
+      case 1: HS_RUN<1, NS>(S, kk); break;
+      default: HS_RUN<6, NS>(S, kk); break;
+    }
   }
   cp_wait<0>();  // no copy may land in smem after the warp has left
 }
