@@ -105,14 +105,26 @@ struct HsCoef {
 #define NG (NR / 2)
 // power ring: a power of two >= TT + NR + 2 rows (slot = row & (PR - 1))
 #define PR (SH_POWER ? ((TT + NR + 2) <= 16 ? 16 : ((TT + NR + 2) <= 32 ? 32 : 64)) : 0)
-#define WARP_FLOATS (SW * (NR + PR))
+// HS_STREAM == 2 ("smem rings"): the level rings live in per-warp shared
+// memory instead of registers (configurations whose TT x TSX register rings
+// exceed the __launch_bounds__ budget); one row per iteration
+#if HS_STREAM == 2
+#define LR (TT * 3)
+#else
+#define LR 0
+#endif
+#define WARP_FLOATS (SW * (NR + PR + LR))
 // staging chunk (floats) and chunks per lane
 #define CW ((TSX % 4) == 0 ? 4 : ((TSX % 2) == 0 ? 2 : 1))
 #define NCH (TSX / CW)
 #define NP2 ((TSX + 1) / 2)
 // rows per stream iteration: loop_unroll_factor_t > 1 unrolls the row stream
 // by two (two independent update chains per level)
+#if HS_STREAM == 2
+#define HS_RPI 1
+#else
 #define HS_RPI ((UNROLL) > 1 ? 2 : 1)
+#endif
 #define COL(v, j) ((j) % 2 == 0 ? (v)[(j) / 2].x : (v)[(j) / 2].y)
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -148,6 +160,7 @@ struct HsStream {
   float* out;
   float* tring;   // NR rows, chunk-major
   float* pring;   // PR rows (SH_POWER)
+  float* lring;   // HS_STREAM == 2: level rings [TT][3] rows, chunk-major
   int lane, gx0, ia, ib, y0, y1, nsteps;
   int cbytes[NCH];   // staging bytes per chunk (0 outside the grid)
   int csrc[NCH];     // global column of each chunk (clamped into the grid)
@@ -176,6 +189,24 @@ __device__ __forceinline__ void lds_pairs(float2 (&v)[NP2], const float* row, in
   }
 #pragma unroll
   for (int q = 0; q < NP2; ++q) v[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
+}
+
+// inverse of lds_pairs: this lane's columns into a chunk-major shared row
+__device__ __forceinline__ void sts_pairs(float* row, const float2 (&v)[NP2], int lane) {
+  float t[TSX];
+#pragma unroll
+  for (int j = 0; j < TSX; ++j) t[j] = COL(v, j);
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    float* p = row + (c * 32 + lane) * CW;
+#if CW == 4
+    *reinterpret_cast<float4*>(p) = make_float4(t[4 * c], t[4 * c + 1], t[4 * c + 2], t[4 * c + 3]);
+#elif CW == 2
+    *reinterpret_cast<float2*>(p) = make_float2(t[2 * c], t[2 * c + 1]);
+#else
+    *p = t[c];
+#endif
+  }
 }
 
 // stage input (and power) row `row` into the rings (no commit)
@@ -373,6 +404,61 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
   hs_store_row(S, ro + 1, f1);
 }
 
+// ---- smem level rings (HS_STREAM == 2) --------------------------------------
+// Same pipeline as hs_stream_iter1, but level k-1's rows a-1, a are read
+// from a 3-row ring in this warp's shared memory and the fresh row (in
+// registers) is written back to it.  Each lane only ever touches its own
+// columns there (E/W still come from shuffles), so no warp sync is needed.
+#if HS_STREAM == 2
+template <int PH, int E, int NS>
+__device__ __forceinline__ void hs_stream_iter_s(const HsStream& S, int i, const HsCoef& kk, const HsK2& k2) {
+  hs_stage_row(S, i + NR - 1);
+  cp_commit();
+  cp_wait<NR - 1>();
+  float2 f0[NP2];
+  lds_pairs(f0, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
+#pragma unroll
+  for (int k = 1; k <= TT; ++k) {
+    if (k > NS) break;
+    const int a = i - k;
+    const int sN = ((PH - k - 1) % 3 + 3) % 3;
+    const int sC = ((PH - k) % 3 + 3) % 3;
+    const int s0 = ((PH - k + 1) % 3 + 3) % 3;
+    float* ring = S.lring + (k - 1) * 3 * SW;
+    sts_pairs(ring + s0 * SW, f0, S.lane);  // level k-1 row a+1
+    float2 N[NP2], Cc[NP2];
+    lds_pairs(N, ring + sN * SW, S.lane);
+    lds_pairs(Cc, ring + sC * SW, S.lane);
+    float wl = __shfl_up_sync(0xffffffffu, COL(Cc, TSX - 1), 1);
+    float er = __shfl_down_sync(0xffffffffu, Cc[0].x, 1);
+    if ((E & 3) == 1) {
+      wl = S.xl ? Cc[0].x : wl;
+      er = S.xr ? COL(Cc, TSX - 1) : er;
+    }
+    float2 pa[NP2];
+    hs_power(pa, S, a);
+    float2 na[NP2];
+    hs_row_update<E>(na, N, Cc, f0, wl, er, pa, (E & 4) && a == 0, (E & 4) && a == GH - 1, S, kk, k2);
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) f0[q] = na[q];
+  }
+  hs_store_row(S, i - NS, f0);
+}
+
+template <int E, int NS>
+__device__ __forceinline__ void hs_stream_run_s(const HsStream& S, const HsCoef& kk) {
+  const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
+                make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
+  for (int i = S.ia; i <= S.ib; i += 3) {
+    hs_stream_iter_s<0, E, NS>(S, i, kk, k2);
+    if (i + 1 > S.ib) break;
+    hs_stream_iter_s<1, E, NS>(S, i + 1, kk, k2);
+    if (i + 2 > S.ib) break;
+    hs_stream_iter_s<2, E, NS>(S, i + 2, kk, k2);
+  }
+}
+#endif
+
 // ---- one row per iteration (loop_unroll_factor_t == 1) --------------------
 // Level k-1 keeps rows a-1, a in a 3-slot ring (row x at (x - ia) mod 3,
 // static for PH = (i - ia) mod 3); the fresh row a+1 arrives from level k-1.
@@ -478,6 +564,7 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
   S.out = out;
   S.tring = smem + wid * WARP_FLOATS;
   S.pring = S.tring + NR * SW;
+  S.lring = S.pring + PR * SW;
   S.gx0 = strip * UW - TA;
   S.nsteps = NS;
   // segments: the first (and, by the host's choice of segh, the last) are
@@ -519,7 +606,9 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
   const bool xalign = (S.gx0 > 0 || (-S.gx0) % TSX == 0) && (S.gx0 + SW <= GW - 1 || (GW - S.gx0) % TSX == 0);
   const bool yedge = S.ia == 0 || S.ib >= GH - 1;
   const int em = (xedge ? (xalign ? 1 : 2) : 0) | (yedge ? 4 : 0);
-#if HS_RPI == 2
+#if HS_STREAM == 2
+#define HS_RUN hs_stream_run_s
+#elif HS_RPI == 2
 #define HS_RUN hs_stream_run
 #else
 #define HS_RUN hs_stream_run1

@@ -302,7 +302,7 @@ class Hotspot(Problem):
         return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
                     UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"],
-                    HS_STREAM=int(self.stream_geometry(cfg) is not None),
+                    HS_STREAM=(self.stream_geometry(cfg) or {}).get("kind", 0),
                     HS_REM=self.iterations % cfg["temporal_tiling_factor"], HS_NR=self.stream_nr(cfg["temporal_tiling_factor"]))
 
     # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
@@ -340,8 +340,12 @@ class Hotspot(Problem):
         # fitted to ptxas counts of the static-depth kernel (tools/hs_regs.py):
         # ~3.5 registers per (level x column), odd TSX pays a scalar tail
         regs = math.ceil(3.5 * t * tsx) + self.STREAM_REG_BASE + (12 * t if tsx % 2 else 0)
+        kind = 1  # level rings in registers
         if regs > budget:
-            return None
+            # level rings in shared memory (HS_STREAM=2): ~5 rows of TSX live
+            kind = 2
+            if self._smem_ring_regs(t, tsx) > budget:
+                return None
         sw = 32 * tsx
         ta = (t + 3) & ~3
         uw = ((sw - ta - t) // 4) * 4
@@ -350,13 +354,14 @@ class Hotspot(Problem):
         nr = self.stream_nr(t)
         pr = (16 if t + nr + 2 <= 16 else (32 if t + nr + 2 <= 32 else 64)) if shp else 0
         wpb = nthreads // 32
-        warp_floats = sw * (nr + pr)
+        warp_floats = sw * (nr + pr + (3 * t if kind == 2 else 0))
         smem = 4 * wpb * warp_floats
         if smem > self.STREAM_SMEM_MAX:
             return None
         nstrips = -(-self.W // uw)
         if blocks_per_sm is None:  # estimate (CPU-side planning / tests)
-            per_warp = -(-min(regs, budget) * 32 // 256) * 256
+            used = min(regs, budget) if kind == 1 else self._smem_ring_regs(t, tsx)
+            per_warp = -(-used * 32 // 256) * 256
             by_regs = 65536 // per_warp // wpb
             by_smem = (228 * 1024) // (smem + 1024) if smem else 32
             blocks_per_sm = max(1, min(by_regs, by_smem, 32, 64 // wpb))
@@ -364,7 +369,13 @@ class Hotspot(Problem):
         nsegs = max(1, min(tsy * wave, self.H // max(8, 2 * t)))
         segh, segh0, nsegs = self._segments(nsegs)
         return dict(sw=sw, ta=ta, uw=uw, segh=segh, segh0=segh0, wpb=wpb, smem=smem, nstrips=nstrips,
-                    nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb), blocks_per_sm=blocks_per_sm)
+                    nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb), blocks_per_sm=blocks_per_sm,
+                    kind=kind)
+
+    def _smem_ring_regs(self, t: int, tsx: int) -> int:
+        """Register estimate of the smem-ring stream kernel (ptxas hoists
+        level loads across the unrolled level loop; conservative fit)."""
+        return 2 * t * tsx + 4 * tsx + self.STREAM_REG_BASE + 8
 
     # top/bottom segment height relative to the others (measured optimum on B200;
     # TSG_HS_EDGE_SEG overrides it for experiments)
@@ -393,8 +404,9 @@ class Hotspot(Problem):
 
     def kernel_mode(self, cfg: dict) -> tuple:
         """(mode, floats per buffer, guard floats, buffers) -- mirrors kernels/hotspot.cu macros."""
-        if self.stream_geometry(cfg) is not None:
-            return "stream", 0, 0, 0
+        geo = self.stream_geometry(cfg)
+        if geo is not None:
+            return ("stream" if geo["kind"] == 1 else "stream_smem"), 0, 0, 0
         bx, by = cfg["block_size_x"], cfg["block_size_y"]
         t, shp = cfg["temporal_tiling_factor"], cfg["sh_power"]
         ew = bx * cfg["tile_size_x"] + 2 * t

@@ -98,14 +98,14 @@ def test_full_size_answer_and_sweep(name, device):
         tgt.close()
 
 
-def _stream_configs(prob, n_per_t=4):
+def _stream_configs(prob, n_per_t=4, mode="stream"):
     """Stream-mode configurations: every T, odd and even TSX, both sh_power
     values, one and two rows per iteration."""
     names = prob.space.param_names
     out = []
     for c in stratified_sample(prob.space, 2000, seed=23, param="temporal_tiling_factor"):
         d = dict(zip(names, c))
-        if prob.kernel_mode(d)[0] == "stream":
+        if prob.kernel_mode(d)[0] == mode:
             key = (d["temporal_tiling_factor"], d["tile_size_x"] % 2, d["sh_power"],
                    d["loop_unroll_factor_t"] > 1)
             if sum(1 for o in out if o[0] == key) < 1:
@@ -130,6 +130,27 @@ def test_hotspot_stream_mode_bit_exact(device):
             assert st is Status.OK, (c, out)
             diff = int(np.sum(out != want))
             assert diff == 0, f"stream {c}: {diff} elements differ"
+    finally:
+        tgt.close()
+
+
+def test_hotspot_stream_smem_mode_bit_exact(device):
+    """Warp-streaming hotspot with the level rings in shared memory (the
+    register-heavy TT x TSX configurations): every T, odd/even TSX, both
+    sh_power values -- bit-exact vs the C oracle."""
+    prob = Hotspot(width=520, height=264, iterations=20)
+    want = K.answer(prob)
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        configs = _stream_configs(prob, mode="stream_smem")
+        assert len(configs) >= 12
+        for c in configs:
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+            st, out = tgt.run_output(c)
+            assert st is Status.OK, (c, out)
+            diff = int(np.sum(out != want))
+            assert diff == 0, f"stream_smem {c}: {diff} elements differ"
     finally:
         tgt.close()
 
