@@ -347,6 +347,7 @@ def our_arm(args, dist: Dist):
             if i % 4 == 0:
                 target.prefetch(configs[i:])
                 sampler.sample()  # clocks/throttle reasons, between configurations
+            target.preload(configs[i + 1:])  # next modules load while this one runs
             obs.append((c, target.execute(c, proto)))
         return obs
 

@@ -135,6 +135,12 @@ class CudaTarget:
         # the driver (measured on B200), which would land inside a sweep
         self._retired: list = []
         self.retire_cap = 256
+        # modules of upcoming configurations are loaded by one helper thread
+        # while the GPU runs the current one (ctypes releases the GIL): an
+        # eager cuModuleLoadData occasionally blocks 10-100 ms in the driver
+        self._loader = ThreadPoolExecutor(max_workers=1, thread_name_prefix="modload")
+        self._preloaded: dict = {}
+        self.preload_depth = 2
         self._pending: "OrderedDict[str, Future]" = OrderedDict()
         self.prefetch_depth = prefetch_depth or 4 * self.compiler.pool._max_workers
         self.stats = {"executed": 0, "gpu_ms": 0.0, "verify_failed": 0}
@@ -189,6 +195,22 @@ class CudaTarget:
                 cfg = dict(zip(names, config))
                 self._pending[key] = self.compiler.submit(self.source_for(cfg), self._options(cfg))
 
+    def preload(self, configs) -> None:
+        """Load the modules of the next ``preload_depth`` configurations in the
+        background (their compilation must already be queued by prefetch)."""
+        for config in configs[: self.preload_depth]:
+            key = config_key(config)
+            if key in self._preloaded or key not in self._pending:
+                continue
+            fut = self._pending[key]
+            self._preloaded[key] = self._loader.submit(self._load_when_compiled, fut)
+
+    def _load_when_compiled(self, fut: Future):
+        res = fut.result()
+        if not res.ok:
+            return None
+        return self.dev.load(res.image)
+
     def _compiled(self, key: str, cfg: dict) -> rt.CompileResult:
         fut = self._pending.pop(key, None)
         if fut is None:
@@ -210,10 +232,13 @@ class CudaTarget:
         if not res.ok:
             return Observation(Status.COMPILE_FAILED, detail=(res.error or res.log)[-2000:])
         t1 = time.perf_counter()
-        rc, mod = self.dev.load(res.image)
+        pre = self._preloaded.pop(key, None)
+        loaded = pre.result() if pre is not None else None
+        rc, mod = loaded if loaded is not None else self.dev.load(res.image)
         if rc != rt.OK:
             return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(mod))
         info["t_load_s"] = time.perf_counter() - t1
+        info["preloaded"] = pre is not None
         try:
             for sym, data in self.problem.constants().items():
                 if mod.set_constant(sym, data) != rt.OK:
@@ -320,6 +345,12 @@ class CudaTarget:
         self._retired.clear()
 
     def close(self):
+        self._loader.shutdown(wait=True)
+        for fut in self._preloaded.values():  # preloaded but never executed
+            r = fut.result()
+            if r is not None and r[0] == rt.OK:
+                r[1].unload()
+        self._preloaded.clear()
         self.flush_modules()
         for b in self.bufs.values():
             b.free()

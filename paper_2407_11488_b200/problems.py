@@ -344,7 +344,9 @@ class Hotspot(Problem):
         if regs > budget:
             # level rings in shared memory (HS_STREAM=2): ~5 rows of TSX live
             kind = 2
-            if self._smem_ring_regs(t, tsx) > budget:
+            # with >= 128 registers per thread it beats the block-tile modes
+            # even where ptxas spills (measured: 5.6 -> 1.3 ms at TSX=T=10)
+            if self._smem_ring_regs(t, tsx) > budget and budget < 128:
                 return None
         sw = 32 * tsx
         ta = (t + 3) & ~3
