@@ -85,23 +85,23 @@ __device__ __forceinline__ unsigned long long umma_desc(unsigned addr, unsigned 
 #ifndef MAJOR_BITS
 #define MAJOR_BITS 0u
 #endif
-#define IDESC ((1u << 4) | (2u << 7) | (2u << 10) | MAJOR_BITS | \
-               ((unsigned)(BN_T >> 3) << 17) | ((unsigned)(BM >> 4) << 24))
+#define IDESC_BASE ((1u << 4) | (2u << 7) | (2u << 10) | MAJOR_BITS | ((unsigned)(BM >> 4) << 24))
+#define IDESC_N(n) (IDESC_BASE | ((unsigned)((n) >> 3) << 17))
 
 __device__ __forceinline__ void umma_tf32(unsigned tmem_d, unsigned long long da, unsigned long long db,
-                                          unsigned accumulate) {
+                                          unsigned idesc, unsigned accumulate) {
 #ifdef MMA_WITH_MASK
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, {%5, %6, %7, %8}, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate), "r"(0u), "r"(0u), "r"(0u), "r"(0u));
 #else
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-      "l"(da), "l"(db), "r"(IDESC), "r"(accumulate));
+      "l"(da), "l"(db), "r"(idesc), "r"(accumulate));
 #endif
 }
 
@@ -111,7 +111,7 @@ __device__ __forceinline__ void umma_commit(unsigned bar) {
 
 extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
-               const __grid_constant__ TmaDesc tma_b) {
+               const __grid_constant__ TmaDesc tma_b, int tiles_m, int n_full) {
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms
   const unsigned base = smem_u32(smem_raw);
@@ -126,8 +126,19 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN_T;
+  // Work items (1-D grid): the first n_full are whole BM x BN_T tiles; the
+  // tiles after them (which would form a partial last wave over the SMs)
+  // are split into two BM x BN_T/2 halves each, so the last wave is as full
+  // as the others (512 whole tiles on 148 SMs would cap at 86.5%).  A half
+  // tile still TMA-loads a full BN_T-row B box (rows past its own 128 are
+  // unused / zero-filled past GN) and runs the MMA with N = BN_T/2.
+  const int item = blockIdx.x;
+  const int tile = item < n_full ? item : n_full + ((item - n_full) >> 1);
+  const int half = item < n_full ? -1 : ((item - n_full) & 1);
+  const int m0 = (tile % tiles_m) * BM;
+  const int bn = half < 0 ? BN_T : BN_T / 2;
+  const int n0 = (tile / tiles_m) * BN_T + (half > 0 ? BN_T / 2 : 0);
+  const unsigned idesc = IDESC_N(bn);
   constexpr int KB = GK / BK;
 
   if (warp == 0 && lane == 0) {
@@ -185,7 +196,7 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
           const unsigned long long da = umma_desc(sa + k * 32, 16, 1024);
           const unsigned long long db = umma_desc(sb + k * 32, 16, 1024);
 #ifndef NO_MMA
-          umma_tf32(tmem, da, db, (kb | k) != 0);
+          umma_tf32(tmem, da, db, idesc, (kb | k) != 0);
 #else
           (void)da;
           (void)db;
@@ -220,7 +231,7 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
     const int m = m0 + q * 32 + lane;
     const unsigned taddr = tmem + ((unsigned)(q * 32) << 16);
 #pragma unroll 1
-    for (int c = 0; c < BN_T; c += 16) {
+    for (int c = 0; c < bn; c += 16) {
       unsigned r[16];
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"

@@ -904,8 +904,14 @@ class GemmTC(Gemm):
         # K-major operands: dim0 = K (contiguous), dim1 = M / N; boxes of 32 K x (128 | BN_T)
         ta = dev.tma_2d_f32(bufs["Ak"], self.K, self.M, self.K * 4, 32, 128, 128)
         tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"], 128)
-        grid = (self.M // 128, self.N // cfg["BN_T"], 1)
-        return [Launch(kernel, grid, (192, 1, 1), [_u64(bufs["out"]), ta, tb], smem=self.smem_bytes(cfg))]
+        tiles_m = self.M // 128
+        tiles = tiles_m * (self.N // cfg["BN_T"])
+        n_sm = int(dev.info.get("sm_count", 148))
+        n_full = (tiles // n_sm) * n_sm  # whole waves of whole tiles; the rest run as halves
+        items = n_full + 2 * (tiles - n_full)
+        return [Launch(kernel, (items, 1, 1), (192, 1, 1),
+                       [_u64(bufs["out"]), ta, tb, C.c_int(tiles_m), C.c_int(n_full)],
+                       smem=self.smem_bytes(cfg))]
 
 
 PROBLEMS = {"convolution": Convolution, "hotspot": Hotspot, "dedispersion": Dedispersion,
