@@ -61,6 +61,10 @@ class Compiler:
         self.cache = cache if cache is not None else rt.CubinCache()
         self._inflight: dict = {}
         self._lock = threading.Lock()
+        # finished compilations kept in memory (a configuration measured again
+        # -- e2e pass, re-tune -- skips the disk cache and the pool round trip)
+        self._done: "OrderedDict[str, Future]" = OrderedDict()
+        self.memory_entries = 1024
         self.stats = {"compiled": 0, "cache_hits": 0, "compile_s": 0.0, "failed": 0}
 
     def _job(self, source: str, options: list, key: str) -> rt.CompileResult:
@@ -82,6 +86,10 @@ class Compiler:
     def submit(self, source: str, options: list) -> Future:
         key = self.cache.key(source, options, None)
         with self._lock:
+            done = self._done.get(key)
+            if done is not None:
+                self._done.move_to_end(key)
+                return done
             fut = self._inflight.get(key)
             if fut is None:
                 fut = self.pool.submit(self._job, source, options, key)
@@ -91,7 +99,11 @@ class Compiler:
 
     def _drop(self, key):
         with self._lock:
-            self._inflight.pop(key, None)
+            fut = self._inflight.pop(key, None)
+            if fut is not None and not fut.cancelled() and fut.exception() is None:
+                self._done[key] = fut
+                while len(self._done) > self.memory_entries:
+                    self._done.popitem(last=False)
 
     def compile(self, source: str, options: list) -> rt.CompileResult:
         return self.submit(source, options).result()
@@ -321,7 +333,7 @@ class CudaTarget:
             self.out.download(out)
             return Status.OK, out
         finally:
-            mod.unload()
+            self._retire(mod)
 
     def _retire(self, mod, key: str | None = None, kernel_name: str | None = None) -> None:
         self._retired.append((mod, key, kernel_name))
