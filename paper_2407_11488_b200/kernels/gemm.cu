@@ -124,7 +124,9 @@ __device__ __forceinline__ constexpr int vidx_n(int i, int t) {
 // registers hold the prefetch (the register round trip cost ~30 registers
 // per thread and capped the larger register tiles' occupancy), one barrier
 // per k-tile.
+#ifndef GEMM_NS
 #define GEMM_NS 3
+#endif
 
 template <int V>
 __device__ __forceinline__ void cp_async_vec(float* dst, const float* src) {

@@ -818,13 +818,13 @@ class Gemm(Problem):
         return self.M * self.N
 
     def problem_defines(self) -> dict:
-        return dict(GM=self.M, GN=self.N, GK=self.K)
+        return dict(GM=self.M, GN=self.N, GK=self.K, GEMM_NS=self.GEMM_NS)
 
     def smem_bytes(self, cfg: dict) -> int:
         # GEMM_NS-deep cp.async ring of staged k-tiles (kernels/gemm.cu)
         return 4 * self.GEMM_NS * cfg["KWG"] * (cfg["MWG"] * cfg["SA"] + cfg["NWG"] * cfg["SB"])
 
-    GEMM_NS = 3
+    GEMM_NS = int(os.environ.get("TSG_GEMM_NS", "3"))
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
