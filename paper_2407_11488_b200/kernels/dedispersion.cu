@@ -29,6 +29,68 @@ __constant__ float d_delay[NCH];
 #define STR2(x) #x
 #define STR(x) STR2(x)
 
+#if (defined(DD_WIN) && DD_WIN) || (defined(DD_STG) && DD_STG)
+// Shared-memory staging: per chunk of CC = 32 channels, each channel's
+// block-wide row segment (the block's 32*TSX samples shifted by the block's
+// FIRST DM, plus BLKSPAN + SPAN samples of DM spread, aligned down to 16 B)
+// is brought in by one TMA bulk copy (cp.async.bulk, issued by warp 0's
+// lanes, completion on the stage's mbarrier), NSTAGE chunks in flight.
+// Warps then read their windows with LDS: 32 consecutive floats at any
+// alignment are one conflict-free wavefront (an unaligned 128-byte global
+// load costs ~2.4 L1 wavefronts and an LSU queue slot).
+#define CC 32
+#if defined(DD_WIN) && DD_WIN
+#define ROWLEN ((32 * TSX + BLKSPAN + SPAN + 4 + 3) & ~3)
+#else
+#define ROWLEN ((BSX * TSX + BLKSPAN + 4 + 3) & ~3)
+#endif
+#ifndef DD_NSTAGE
+#define DD_NSTAGE 5
+#endif
+#define NSTAGE DD_NSTAGE
+
+__device__ __forceinline__ unsigned dd_smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void dd_mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void dd_mbar_arrive(unsigned long long* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dd_smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void dd_mbar_expect(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void dd_mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(dd_smem_u32(b)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void dd_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dd_smem_u32(dst)), "l"(src), "r"(bytes), "r"(dd_smem_u32(b))
+      : "memory");
+}
+
+// warp 0: stage chunk t (channels t*CC ..) into `stage`
+__device__ __forceinline__ void dd_issue_chunk(const float* __restrict__ in, float* stage, unsigned long long* bar,
+                                               int t, int sb, float dmb, int lane, const float* sdelay) {
+  const int ch = t * CC + lane;
+  const int nvalid = NCH - t * CC < CC ? NCH - t * CC : CC;
+  if (lane == 0) dd_mbar_expect(bar, (unsigned)(nvalid * ROWLEN * 4));
+  __syncwarp();
+  if (ch < NCH) {
+    const int shb = __float2int_rz(__fmul_rn(dmb, sdelay[ch]));
+    const int a = (sb + shb) & ~3;
+    dd_bulk(stage + lane * ROWLEN, in + (size_t)ch * IN_PITCH + a, ROWLEN * 4, bar);
+  }
+}
+
+#endif  // staging
+
 #if defined(DD_WIN) && DD_WIN
 // ============================================================================
 // WINDOW mode (host-selected for block_size_x == 32 with strided samples and
@@ -132,58 +194,6 @@ __device__ __forceinline__ void dd_dispatch(DdWin& st, int idx, const float* p) 
     dd_switch<DD_S2, (SPAN >= 2 ? DD_S3 - DD_S2 : 0)>(st, idx, p);
   } else {
     dd_switch<DD_S3, NVALID - DD_S3>(st, idx, p);
-  }
-}
-
-// Shared-memory staging: per chunk of CC = 32 channels, each channel's
-// block-wide row segment (the block's 32*TSX samples shifted by the block's
-// FIRST DM, plus BLKSPAN + SPAN samples of DM spread, aligned down to 16 B)
-// is brought in by one TMA bulk copy (cp.async.bulk, issued by warp 0's
-// lanes, completion on the stage's mbarrier), NSTAGE chunks in flight.
-// Warps then read their windows with LDS: 32 consecutive floats at any
-// alignment are one conflict-free wavefront (an unaligned 128-byte global
-// load costs ~2.4 L1 wavefronts and an LSU queue slot).
-#define CC 32
-#define ROWLEN ((32 * TSX + BLKSPAN + SPAN + 4 + 3) & ~3)
-#define NSTAGE 5
-
-__device__ __forceinline__ unsigned dd_smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void dd_mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void dd_mbar_arrive(unsigned long long* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(dd_smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void dd_mbar_expect(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(dd_smem_u32(b)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void dd_mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT_%=;\n}" ::"r"(dd_smem_u32(b)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void dd_bulk(void* dst, const void* src, unsigned bytes, unsigned long long* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          dd_smem_u32(dst)), "l"(src), "r"(bytes), "r"(dd_smem_u32(b))
-      : "memory");
-}
-
-// warp 0: stage chunk t (channels t*CC ..) into `stage`
-__device__ __forceinline__ void dd_issue_chunk(const float* __restrict__ in, float* stage, unsigned long long* bar,
-                                               int t, int sb, float dmb, int lane, const float* sdelay) {
-  const int ch = t * CC + lane;
-  const int nvalid = NCH - t * CC < CC ? NCH - t * CC : CC;
-  if (lane == 0) dd_mbar_expect(bar, (unsigned)(nvalid * ROWLEN * 4));
-  __syncwarp();
-  if (ch < NCH) {
-    const int shb = __float2int_rz(__fmul_rn(dmb, sdelay[ch]));
-    const int a = (sb + shb) & ~3;
-    dd_bulk(stage + lane * ROWLEN, in + (size_t)ch * IN_PITCH + a, ROWLEN * 4, bar);
   }
 }
 
@@ -309,6 +319,94 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       if (sa < NSAMP) o[sa] = v.x;
       if (2 * q + 1 < TSX && sbb < NSAMP) o[sbb] = v.y;
     }
+  }
+}
+
+#elif defined(DD_STG) && DD_STG
+// ============================================================================
+// STAGED generic mode (any block shape; the host selects it when the staged
+// rows fit in shared memory): the same per-thread (sample, DM) tiles and
+// channel order as the plain generic kernel, but every channel's block-wide
+// row segment arrives by TMA bulk copy into a 5-stage ring (as in window
+// mode) and the adds read it with LDS: the input stream is prefetched
+// instead of each load waiting on L2/HBM (the plain kernel is latency
+// bound), and 32 consecutive floats at any alignment are one smem wavefront.
+// ============================================================================
+extern "C" __global__ void __launch_bounds__(BSX * BSY)
+dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float dm_first,
+                    float dm_step) {
+  extern __shared__ __align__(128) float smem[];
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + NSTAGE * CC * ROWLEN);
+  unsigned long long* empty = bars + NSTAGE;
+  float* sdelay = reinterpret_cast<float*>(empty + NSTAGE);
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tid = ty * BSX + tx, lane = tid & 31, w = tid >> 5;
+  constexpr int NT = BSX * BSY, NW = (NT + 31) / 32;
+  const unsigned wmask = (NT - 32 * w >= 32) ? 0xffffffffu : ((1u << (NT - 32 * w)) - 1u);
+  const int sb = (int)blockIdx.y * (BSX * TSX);   // block's first sample
+  const int db0 = (int)blockIdx.x * (BSY * TSY);  // block's first DM (< NDM)
+  const float dmb = __fadd_rn(dm_first, __fmul_rn((float)db0, dm_step));
+  int so[TSX];  // sample offsets within the block
+#pragma unroll
+  for (int i = 0; i < TSX; ++i) so[i] = STX ? tx + i * BSX : tx * TSX + i;
+  int d[TSY];
+  float dmv[TSY];
+#pragma unroll
+  for (int j = 0; j < TSY; ++j) {
+    d[j] = db0 + (STY ? ty + j * BSY : ty * TSY + j);
+    const int dc = d[j] < NDM ? d[j] : NDM - 1;  // overshoot rows compute a valid DM, never stored
+    dmv[j] = __fadd_rn(dm_first, __fmul_rn((float)dc, dm_step));
+  }
+  for (int c = tid; c < NCH; c += NT) sdelay[c] = d_delay[c];
+  if (tid == 0) {
+#pragma unroll
+    for (int b = 0; b < NSTAGE; ++b) {
+      dd_mbar_init(bars + b, 1);
+      dd_mbar_init(empty + b, NW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int nchunks = (NCH + CC - 1) / CC;
+  if (w == 0)
+    for (int t = 0; t < NSTAGE && t < nchunks; ++t)
+      dd_issue_chunk(in, smem + t * CC * ROWLEN, bars + t, t, sb, dmb, lane, sdelay);
+  float acc[TSY][TSX];
+#pragma unroll
+  for (int j = 0; j < TSY; ++j)
+#pragma unroll
+    for (int i = 0; i < TSX; ++i) acc[j][i] = 0.f;
+  for (int t = 0; t < nchunks; ++t) {
+    const int stg = t % NSTAGE;
+    dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
+    const float* srow = smem + stg * CC * ROWLEN;
+    const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
+#pragma unroll 2
+    for (int c = 0; c < nch; ++c, srow += ROWLEN) {
+      const float dl = sdelay[t * CC + c];
+      const int shb = __float2int_rz(__fmul_rn(dmb, dl));
+      const float* row = srow + ((sb + shb) & 3) - shb;  // row[sh + so] = in[ch][sb + so + sh]
+#pragma unroll
+      for (int j = 0; j < TSY; ++j) {
+        const float* p = row + __float2int_rz(__fmul_rn(dmv[j], dl));
+#pragma unroll
+        for (int i = 0; i < TSX; ++i) acc[j][i] = __fadd_rn(acc[j][i], p[so[i]]);
+      }
+    }
+    __syncwarp(wmask);
+    if (lane == 0) dd_mbar_arrive(empty + stg);
+    if (w == 0 && t + NSTAGE < nchunks) {
+      dd_mbar_wait(empty + stg, (t / NSTAGE) & 1);
+      dd_issue_chunk(in, smem + stg * CC * ROWLEN, bars + stg, t + NSTAGE, sb, dmb, lane, sdelay);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < TSY; ++j) {
+    if (d[j] >= NDM) continue;
+    float* o = out + (size_t)d[j] * NSAMP;
+#pragma unroll
+    for (int i = 0; i < TSX; ++i)
+      if (sb + so[i] < NSAMP) o[sb + so[i]] = acc[j][i];
   }
 }
 

@@ -660,6 +660,10 @@ class Dedispersion(Problem):
         span = self.window_span(cfg)
         if span is not None:
             d.update(DD_WIN=1, SPAN=span, BLKSPAN=self.block_span(cfg))
+        else:
+            ns = self.staged_stages(cfg)
+            if ns:
+                d.update(DD_STG=1, DD_NSTAGE=ns, BLKSPAN=self.block_span(cfg))
         return d
 
     DD_ASM_MARKER = "// @DD_ASM_DISPATCH@"
@@ -702,10 +706,40 @@ class Dedispersion(Problem):
     def smem_bytes(self, cfg: dict) -> int:
         span = self.window_span(cfg)
         if span is None:
-            return 0
+            ns = self.staged_stages(cfg)
+            return self._staged_smem(cfg, ns) if ns else 0
         rowlen = (32 * cfg["tile_size_x"] + self.block_span(cfg) + span + 4 + 3) & ~3
         npat = 1 << (cfg["tile_size_y"] - 1)
         return 4 * self.DD_STAGES * self.DD_CC * rowlen + 16 * self.DD_STAGES + 4 * self.NCH + npat
+
+    # staged generic mode (kernels/dedispersion.cu DD_STG) for non-window
+    # configurations with enough work per staged row: >= 4 threads and >= 12
+    # samples per block row, >= 8 outputs per thread.  Measured on B200
+    # (46-configuration A/B, profiles/round1/dd_staged_ab.md): those run
+    # 1.0-2.0x faster staged; narrower blocks (1-2 threads in x, few
+    # samples per block) re-stage nearly the same DM-spread rows per handful
+    # of outputs and run up to 4x slower, so they keep the plain kernel.
+    # TSG_DD_STG=0 forces the plain kernel everywhere, =all staged wherever
+    # it fits (A/B measurements).
+    STAGED_ENV = "TSG_DD_STG"
+    STAGED_SMEM_MAX = 200 * 1024
+
+    def _staged_smem(self, cfg: dict, ns: int) -> int:
+        rowlen = (cfg["block_size_x"] * cfg["tile_size_x"] + self.block_span(cfg) + 4 + 3) & ~3
+        return 4 * ns * self.DD_CC * rowlen + 16 * ns + 4 * self.NCH
+
+    def staged_stages(self, cfg: dict) -> int:
+        """Ring depth of the staged generic kernel (largest <= 5 that fits), 0 = plain kernel."""
+        mode = os.environ.get(self.STAGED_ENV, "1")
+        if mode == "0":
+            return 0
+        if mode != "all" and not (cfg["block_size_x"] >= 4 and cfg["block_size_x"] * cfg["tile_size_x"] >= 12
+                                  and cfg["tile_size_x"] * cfg["tile_size_y"] >= 8):
+            return 0
+        for ns in range(self.DD_STAGES, 1, -1):
+            if self._staged_smem(cfg, ns) <= self.STAGED_SMEM_MAX:
+                return ns
+        return 0
 
     _spans: dict = {}
 

@@ -240,3 +240,36 @@ def test_dedispersion_window_mode_bit_exact(device, shape):
             assert diff == 0, f"window {c}: {diff} elements differ"
     finally:
         tgt.close()
+
+
+@pytest.mark.parametrize("staged", ["all", "0"], ids=["staged", "plain"])
+def test_dedispersion_generic_modes_bit_exact(device, monkeypatch, staged):
+    """Generic dedispersion, both kernels: the TMA-staged one (5..2-deep
+    ring sized to the block's DM spread; TSG_DD_STG=all forces it wherever
+    it fits) and the plain load-per-add one (TSG_DD_STG=0).  Partial last warp (1x40 threads), channel tail chunk,
+    partial DM block, ragged sample tail, strided and contiguous tiles."""
+    monkeypatch.setenv(Dedispersion.STAGED_ENV, staged)
+    prob = Dedispersion(channels=200, samples=3001, dms=300, dm_step=0.05, ch_bw_mhz=1.0)
+    want = K.answer(prob)
+    names = prob.space.param_names
+    configs = [(1, 40, 1, 1, 0, 0), (2, 48, 3, 4, 1, 1), (16, 64, 4, 3, 1, 0), (4, 256, 2, 8, 0, 1),
+               (8, 128, 3, 7, 1, 1), (32, 32, 4, 2, 0, 1), (1, 256, 4, 8, 0, 0)]
+    configs += stratified_sample(prob.space, 24, seed=5, param="block_size_x")
+    tgt = CudaTarget(prob, device=device, answer=want)
+    try:
+        n_staged = 0
+        for c in configs:
+            cfg = dict(zip(names, c))
+            if prob.window_span(cfg) is not None:
+                continue
+            n_staged += bool(prob.staged_stages(cfg))
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+            st, out = tgt.run_output(c)
+            assert st is Status.OK, (c, out)
+            diff = int(np.sum(out != want))
+            assert diff == 0, f"generic {c} staged={staged}: {diff} elements differ"
+        assert n_staged == (0 if staged == "0" else len([c for c in configs
+                                                           if prob.window_span(dict(zip(names, c))) is None]))
+    finally:
+        tgt.close()
