@@ -1,0 +1,123 @@
+"""The ``tune`` command line (SURVEY §8f row 2; ref ts/cli.py:58-139, :277-283).
+
+Runs on the simulated (replay) backend with the reference's golden
+strategy records, so the command's caches and printed results can be
+checked against the traces the reference itself produced; plus resume
+from a torn observation log and the exit-code contract.
+"""
+
+import json
+import subprocess
+import sys
+
+import pytest
+from click.testing import CliRunner
+
+from paper_2407_11488_b200.cli import cli
+from paper_2407_11488_b200.paramspace import config_key, parse_space_spec
+from paper_2407_11488_b200.store import read_cache, write_cache
+from test_strategies import golden_backend
+
+
+def _setup(golden, tmp_path, which=0):
+    rec = golden["strategies"][which]
+    s, be = golden_backend(rec)
+    spec = tmp_path / "space.spec"
+    spec.write_text(rec["text"])
+    src = tmp_path / "replay.json"
+    write_cache(be.cache, src)
+    return rec, s, spec, src
+
+
+def test_tune_brute_matches_reference_brute_force(golden, tmp_path):
+    rec, s, spec, src = _setup(golden, tmp_path)
+    out = tmp_path / "out.json"
+    kt = tmp_path / "kt.json"
+    r = CliRunner().invoke(cli, ["tune", "--space", str(spec), "--backend", f"sim:{src}", "--out", str(out),
+                                 "--kt-out", str(kt)])
+    assert r.exit_code == 0, r.output
+    cache = read_cache(out)
+    assert sorted(cache.records) == sorted(s_key for s_key in json.loads(rec["cache_text"])["records"])
+    assert cache.metadata == {"strategy": "brute", "seed": "0"}
+    want_best = rec["brute_best"]
+    if want_best:
+        assert f"best config : {want_best}" in r.output
+    assert json.loads(kt.read_text())["tune_params_keys"] == list(s.param_names)
+
+
+def test_tune_random_and_local_traces(golden, tmp_path):
+    rec, s, spec, src = _setup(golden, tmp_path)
+    checked = 0
+    for run in rec["runs"]:
+        if run["kind"] not in ("random", "greedy"):
+            continue
+        out = tmp_path / f"{run['kind']}.json"
+        strategy = "random" if run["kind"] == "random" else "local"
+        r = CliRunner().invoke(cli, ["tune", "--space", str(spec), "--backend", f"sim:{src}", "--out", str(out),
+                                     "--strategy", strategy, "--budget", str(run["budget"]),
+                                     "--seed", str(run["seed"])])
+        assert r.exit_code == 0, r.output
+        assert sorted(read_cache(out).records) == sorted(run["trace"])
+        assert f"evaluations : {len(run['trace'])}" in r.output
+        if run["best"]:
+            assert f"best config : {run['best']}" in r.output
+        for note in run["notes"]:
+            assert f"note        : {note}" in r.output
+        checked += 1
+    assert checked >= 2
+
+
+def test_tune_resume_from_torn_log(golden, tmp_path):
+    rec, s, spec, src = _setup(golden, tmp_path)
+    log = tmp_path / "obs.jsonl"
+    args = ["tune", "--space", str(spec), "--backend", f"sim:{src}", "--resume", str(log), "--chunk", "3"]
+    r = CliRunner().invoke(cli, args + ["--out", str(tmp_path / "a.json")])
+    assert r.exit_code == 0, r.output
+    lines = log.read_text().splitlines()
+    n = s.space_size()
+    assert len(lines) == n
+    # keep a third of the log plus a torn half line, as a crash would
+    keep = lines[: n // 3]
+    log.write_text("\n".join(keep) + "\n" + lines[n // 3][: 10])
+    r = CliRunner().invoke(cli, args + ["--out", str(tmp_path / "b.json")])
+    assert r.exit_code == 0, r.output
+    good = [json.loads(x) for x in log.read_text().splitlines() if x.startswith("{") and x.endswith("}")]
+    assert sorted(d["key"] for d in good) == sorted(json.loads(x)["key"] for x in lines)
+    a, b = read_cache(tmp_path / "a.json"), read_cache(tmp_path / "b.json")
+    assert a.records == b.records
+    assert sorted(a.records) == sorted(config_key(c) for c in s.enumerate_configs())
+
+
+def test_exit_codes(golden, tmp_path):
+    rec, s, spec, src = _setup(golden, tmp_path)
+    # domain error -> "error: <Type>: ..." and exit 1 (ref ts/cli.py:277-283)
+    p = subprocess.run([sys.executable, "-m", "paper_2407_11488_b200", "tune", "--space",
+                        str(tmp_path / "missing.spec"), "--backend", f"sim:{src}", "--out",
+                        str(tmp_path / "x.json")], capture_output=True, text=True, timeout=120)
+    assert p.returncode == 1 and p.stderr.startswith("error: SpecValidationError"), p.stderr
+    # usage errors -> exit 2
+    r = CliRunner().invoke(cli, ["tune", "--space", str(spec), "--backend", "gpu:x", "--out", "y.json"])
+    assert r.exit_code == 2
+    r = CliRunner().invoke(cli, ["tune", "--space", str(spec), "--backend", f"sim:{src}", "--out", "y.json",
+                                 "--devices", "2"])
+    assert r.exit_code == 2
+    assert parse_space_spec(rec["text"]).space_size() == s.space_size()
+
+
+@pytest.mark.gpu
+def test_tune_cuda_backend(tmp_path):
+    """``--backend cuda:<kernel>`` end to end on the GPU: random search over
+    the convolution space, then a resumed brute-force slice of the same log."""
+    out = tmp_path / "conv.json"
+    r = CliRunner().invoke(cli, ["tune", "--space", "convolution", "--backend", "cuda:convolution",
+                                 "--strategy", "random", "--budget", "6", "--seed", "1", "--out", str(out),
+                                 "--kt-out", str(tmp_path / "conv_kt.json")])
+    assert r.exit_code == 0, (r.output, r.exception)
+    cache = read_cache(out)
+    assert len(cache.records) == 6
+    assert "B200" in cache.device_name
+    assert any(o.ok for o in cache.records.values())
+    assert "best config : " in r.output
+    r = CliRunner().invoke(cli, ["tune", "--space", "dedispersion", "--backend", "cuda:convolution",
+                                 "--out", str(tmp_path / "bad.json")])
+    assert r.exit_code != 0 and "does not match" in str(r.exception)
