@@ -449,10 +449,14 @@ def our_arm(args, dist: Dist):
         dist.barrier()
         dev.mark(2)
         e2e_cfg = 0
+        brk = {"h2d_s": 0.0, "configs_s": 0.0, "d2h_s": 0.0}
         for cs in timed_sets:
+            t0 = time.perf_counter()
             for k, arr in pinned.items():
                 target.bufs[k].upload(arr)
+            t1 = time.perf_counter()
             obs = run_step(cs)
+            t2 = time.perf_counter()
             e2e_cfg += len(cs)
             okb = [(c, o) for c, o in obs if o.ok]
             if okb:
@@ -460,12 +464,17 @@ def our_arm(args, dist: Dist):
                 st, out = target.run_output(bc)
                 if st.value == "ok":
                     out_host[:] = out
+            t3 = time.perf_counter()
+            brk["h2d_s"] += t1 - t0
+            brk["configs_s"] += t2 - t1
+            brk["d2h_s"] += t3 - t2
         dev.mark(3)
         e2e_ms = dist.max(dev.elapsed_ms(2, 3))
         e2e = {"value": round(dist.sum(e2e_cfg) / (e2e_ms / 1000.0), 3), "unit": "configs/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_host.nbytes),
                "path": "CudaTarget.execute per config (C-ABI tsg_run_timed) + inputs H2D from pinned "
-                       "host memory + best output D2H, every step"}
+                       "host memory + best output D2H, every step",
+               "host_breakdown_s": {k: round(v, 4) for k, v in brk.items()}}
         for arr in list(pinned.values()) + [out_host]:
             dev.lib.tsg_host_unregister(arr.ctypes.data)
 
