@@ -342,14 +342,11 @@ def our_arm(args, dist: Dist):
     space = prob.space
 
     def run_step(configs):
-        obs = []
-        for i, c in enumerate(configs):
-            if i % 4 == 0:
-                target.prefetch(configs[i:])
-                sampler.sample()  # clocks/throttle reasons, between configurations
-            target.preload(configs[i + 1:])  # next modules load while this one runs
-            obs.append((c, target.execute(c, proto)))
-        return obs
+        # pipelined: configuration i+1 is enqueued before i is waited for
+        # (CudaTarget.execute_many); compilation prefetch and module preload
+        # run ahead inside it; clocks/throttle reasons sampled every 4 configs
+        return list(target.execute_many(configs, proto,
+                                        on_config=lambda i: sampler.sample() if i % 4 == 0 else None))
 
     # nvidia-smi is started here, BEFORE the warm-up: its NVML start-up holds
     # driver locks for ~0.3 s and would otherwise stall the first timed

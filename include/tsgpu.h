@@ -158,6 +158,25 @@ int tsg_run_timed(tsg_ctx* ctx, const tsg_launch_t* seq, int n_launch, int warmu
  * roofline accounting of the dominant kernel. */
 int tsg_last_launch_times(tsg_ctx* ctx, float* times_ms, int n_launch);
 
+/* Pipelined protocol (new; same measurement as tsg_run_timed).  Submit
+ * enqueues, into slot 0..TSG_SLOTS-1, the output poison (NaN fill of
+ * `poison_out`, n_out floats; 0 = none), the warm-up + timed runs and,
+ * when `ref` != 0, the on-device comparison of poison_out against ref --
+ * and returns without waiting.  Collect waits (watchdog `timeout_ms`) and
+ * returns the per-run times, the last run's per-launch times (n_launch
+ * floats, may be NULL) and the comparison.  A slot must be collected
+ * before it is submitted again; tsg_slot_reset drops a failed submission.
+ * Two slots let the host prepare configuration i+1 while the device runs
+ * configuration i (replaces the per-configuration synchronisations of
+ * tsg_memset32 + tsg_run_timed + tsg_compare_f32). */
+#define TSG_SLOTS 2
+int tsg_submit_timed(tsg_ctx* ctx, int slot, const tsg_launch_t* seq, int n_launch, int warmup, int runs,
+                     int flush_l2, uint64_t poison_out, size_t n_out, uint64_t ref, double rtol,
+                     double atol);
+int tsg_collect(tsg_ctx* ctx, int slot, double timeout_ms, float* times_ms, float* launch_ms, int n_launch,
+                double* max_abs_err, double* max_abs_ref, uint64_t* n_bad, uint64_t* n_nonfinite);
+int tsg_slot_reset(tsg_ctx* ctx, int slot);
+
 /* TMA: encode a 2-D fp32 tensor map (CUtensorMap, 128 bytes written to
  * `desc128`) for `cp.async.bulk.tensor` in kernels that take it as a
  * __grid_constant__ parameter.  dim0 is contiguous; stride1_bytes is the

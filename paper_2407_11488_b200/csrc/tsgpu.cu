@@ -73,6 +73,14 @@ struct tsg_ctx {
   bool poisoned = false;
   std::vector<float> last_launch_ms;
   CUevent marks[16] = {};
+  // pipelined submission slots (tsg_submit_timed / tsg_collect)
+  struct Slot {
+    std::vector<CUevent> ev;  // [2*total run brackets][n+1 launch marks][done]
+    CUdeviceptr scratch = 0;  // compare accumulators
+    unsigned long long* host = nullptr;  // pinned copy of the accumulators
+    int warmup = 0, runs = 0, n = 0;
+    bool verify = false, active = false;
+  } slots[TSG_SLOTS];
   tsg_device_info_t info{};
 };
 
@@ -312,6 +320,14 @@ int tsg_destroy(tsg_ctx* c) {
     for (CUevent e : c->events) cuEventDestroy(e);
     if (c->flush_buf) cuMemFree(c->flush_buf);
     if (c->scratch) cuMemFree(c->scratch);
+    for (auto& sl : c->slots) {
+      for (CUevent e : sl.ev) cuEventDestroy(e);
+      if (sl.scratch) cuMemFree(sl.scratch);
+      if (sl.host) {
+        cuMemHostUnregister(sl.host);
+        free(sl.host);
+      }
+    }
     cuStreamDestroy(c->stream);
   }
   cuDevicePrimaryCtxRelease(c->dev);
@@ -562,6 +578,120 @@ int tsg_run_timed(tsg_ctx* c, const tsg_launch_t* seq, int n, int warmup, int ru
   }
   c->last_launch_ms.assign(n, 0.f);
   for (int i = 0; i < n; ++i) cuEventElapsedTime(&c->last_launch_ms[i], lev[i], lev[i + 1]);
+  return TSG_OK;
+}
+
+// ---- pipelined measurement -------------------------------------------------
+// tsg_submit_timed enqueues one configuration's whole protocol -- output
+// poison, warm-up + timed runs (flushes, events), on-device comparison and
+// the accumulator copy to pinned host memory -- and returns WITHOUT waiting;
+// tsg_collect waits for that slot and reads it.  With two slots the host
+// prepares and enqueues configuration i+1 while the GPU still runs i, so
+// the stream never idles between configurations (module load, constant
+// upload, argument packing and the Python bookkeeping all overlap device
+// work).  Per-run times are still event pairs around each run on the one
+// stream: the measured quantity is unchanged.
+int tsg_submit_timed(tsg_ctx* c, int slot, const tsg_launch_t* seq, int n, int warmup, int runs, int flush,
+                     uint64_t poison_out, size_t n_out, uint64_t ref, double rtol, double atol) {
+  int s = make_current(c);
+  if (s) return s;
+  if (slot < 0 || slot >= TSG_SLOTS) return fail(TSG_ERR_ARG, "slot out of range");
+  if (runs < 1 || warmup < 0 || n < 1) return fail(TSG_ERR_ARG, "bad protocol");
+  auto& sl = c->slots[slot];
+  if (sl.active) return fail(TSG_ERR_ARG, "slot still in flight (collect it first)");
+  const int total = warmup + runs;
+  const size_t need = 2 * (size_t)total + n + 2;
+  while (sl.ev.size() < need) {
+    CUevent e;
+    CUresult r = cuEventCreate(&e, CU_EVENT_DEFAULT);
+    if (r != CUDA_SUCCESS) return fail(TSG_ERR_SETUP, "cuEventCreate: " + cu_msg(r));
+    sl.ev.push_back(e);
+  }
+  if (!sl.scratch) {
+    CUresult r = cuMemAlloc(&sl.scratch, 64);
+    if (r != CUDA_SUCCESS) return fail(TSG_ERR_SETUP, "slot scratch: " + cu_msg(r));
+    void* h = nullptr;
+    if (posix_memalign(&h, 4096, 4096)) return fail(TSG_ERR_SETUP, "slot host buffer");
+    memset(h, 0, 4096);
+    r = cuMemHostRegister(h, 4096, 0);
+    if (r != CUDA_SUCCESS) {
+      free(h);
+      return fail(TSG_ERR_SETUP, "slot host register: " + cu_msg(r));
+    }
+    sl.host = static_cast<unsigned long long*>(h);
+  }
+  CUevent* ev = sl.ev.data();
+  CUevent* lev = ev + 2 * total;
+  CUresult r;
+  if (poison_out && (r = cuMemsetD32Async((CUdeviceptr)poison_out, 0x7FC00000u, n_out, c->stream)) != CUDA_SUCCESS)
+    return fail(TSG_ERR_RUNTIME, "poison: " + cu_msg(r));
+  for (int k = 0; k < total; ++k) {
+    if (flush && (s = flush_l2(c))) return s;
+    cuEventRecord(ev[2 * k], c->stream);
+    const bool last = (k == total - 1);
+    for (int i = 0; i < n; ++i) {
+      if (last) cuEventRecord(lev[i], c->stream);
+      if ((s = launch_one(c, seq[i]))) return s;  // rejected launch: nothing of this slot waits
+    }
+    if (last) cuEventRecord(lev[n], c->stream);
+    cuEventRecord(ev[2 * k + 1], c->stream);
+  }
+  if (ref) {
+    cuMemsetD32Async(sl.scratch, 0, 8, c->stream);
+    compare_f32_kernel<<<c->info.sm_count * 8, 256, 0, (cudaStream_t)c->stream>>>(
+        (const float*)poison_out, (const float*)ref, n_out, (float)rtol, (float)atol,
+        (unsigned long long*)sl.scratch);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(TSG_ERR_RUNTIME, std::string("compare: ") + cudaGetErrorString(e));
+    c->launches.fetch_add(1, std::memory_order_relaxed);
+    if ((r = cuMemcpyDtoHAsync(sl.host, sl.scratch, 32, c->stream)) != CUDA_SUCCESS)
+      return fail(TSG_ERR_RUNTIME, "compare copy: " + cu_msg(r));
+  }
+  cuEventRecord(ev[need - 1], c->stream);
+  sl.warmup = warmup;
+  sl.runs = runs;
+  sl.n = n;
+  sl.verify = ref != 0;
+  sl.active = true;
+  return TSG_OK;
+}
+
+int tsg_collect(tsg_ctx* c, int slot, double timeout_ms, float* times_ms, float* launch_ms, int n_launch,
+                double* max_abs_err, double* max_abs_ref, uint64_t* n_bad, uint64_t* n_nonfinite) {
+  int s = make_current(c);
+  if (s) return s;
+  if (slot < 0 || slot >= TSG_SLOTS) return fail(TSG_ERR_ARG, "slot out of range");
+  auto& sl = c->slots[slot];
+  if (!sl.active) return fail(TSG_ERR_ARG, "slot not submitted");
+  sl.active = false;
+  const int total = sl.warmup + sl.runs;
+  CUevent* ev = sl.ev.data();
+  if ((s = wait_stream(c, ev[2 * (size_t)total + sl.n + 1], timeout_ms))) return s;
+  for (int k = sl.warmup; k < total; ++k) cuEventElapsedTime(&times_ms[k - sl.warmup], ev[2 * k], ev[2 * k + 1]);
+  CUevent* lev = ev + 2 * total;
+  c->last_launch_ms.assign(sl.n, 0.f);
+  for (int i = 0; i < sl.n; ++i) cuEventElapsedTime(&c->last_launch_ms[i], lev[i], lev[i + 1]);
+  if (launch_ms)
+    for (int i = 0; i < n_launch; ++i) launch_ms[i] = i < sl.n ? c->last_launch_ms[i] : 0.f;
+  if (sl.verify) {
+    const unsigned long long* acc = sl.host;
+    unsigned u0 = (unsigned)acc[0], u1 = (unsigned)acc[1];
+    float f0, f1;
+    memcpy(&f0, &u0, 4);
+    memcpy(&f1, &u1, 4);
+    if (max_abs_err) *max_abs_err = f0;
+    if (max_abs_ref) *max_abs_ref = f1;
+    if (n_bad) *n_bad = acc[2];
+    if (n_nonfinite) *n_nonfinite = acc[3];
+  }
+  return TSG_OK;
+}
+
+/* Drop a slot whose submission failed part-way (after the stream drained). */
+int tsg_slot_reset(tsg_ctx* c, int slot) {
+  if (!c) return fail(TSG_ERR_ARG, "null context");
+  if (slot < 0 || slot >= TSG_SLOTS) return fail(TSG_ERR_ARG, "slot out of range");
+  c->slots[slot].active = false;
   return TSG_OK;
 }
 

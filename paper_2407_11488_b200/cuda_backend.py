@@ -156,6 +156,7 @@ class CudaTarget:
         self._pending: "OrderedDict[str, Future]" = OrderedDict()
         self.prefetch_depth = prefetch_depth or 4 * self.compiler.pool._max_workers
         self.stats = {"executed": 0, "gpu_ms": 0.0, "verify_failed": 0}
+        self._slots_inflight: list = []  # execute_many: enqueued, not yet collected
 
     # -- answer ------------------------------------------------------------------
     def _load(self, image: bytes):
@@ -308,6 +309,148 @@ class CudaTarget:
         self.stats["gpu_ms"] += sum(times)
         return Observation(Status.OK, times_ms=tuple(times),
                            time_ms=aggregate_times(protocol, times))
+
+    # -- pipelined protocol (same measurement, no idle device between configs) --
+    def _prepare(self, config, info: dict):
+        """Compile wait, module, constants, smem opt-in, launch list: the
+        host-side part of one configuration.  Returns (mod, launches) or an
+        Observation for a configuration that fails before any launch."""
+        cfg = dict(zip(self.problem.space.param_names, config))
+        key = config_key(config)
+        t0 = time.perf_counter()
+        res = self._compiled(key, cfg)
+        info["compile_wait_s"] = time.perf_counter() - t0
+        if not res.ok:
+            return Observation(Status.COMPILE_FAILED, detail=(res.error or res.log)[-2000:])
+        t1 = time.perf_counter()
+        pre = self._preloaded.pop(key, None)
+        loaded = pre.result() if pre is not None else None
+        rc, mod = loaded if loaded is not None else self.dev.load(res.image)
+        if rc != rt.OK:
+            return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(mod))
+        info["t_load_s"] = time.perf_counter() - t1
+        info["preloaded"] = pre is not None
+        for sym, data in self.problem.constants().items():
+            if mod.set_constant(sym, data) != rt.OK:
+                self._retire(mod, key, self.problem.kernel_name)
+                return Observation(Status.RUNTIME_FAILED, detail=rt.last_error())
+        kern = mod.function(self.problem.kernel_name)
+        smem = self.problem.smem_bytes(cfg)
+        if smem > 48 * 1024 and kern.set_max_dynamic_smem(smem) != rt.OK:
+            self._retire(mod, key, self.problem.kernel_name)
+            return Observation(Status.INVALID, detail=rt.last_error())
+        if smem > 0:
+            kern.set_smem_carveout(100)
+        info["smem_bytes"] = smem
+        launches = self.problem.launches(cfg, kern, self.bufs)
+        info["t_setup_s"] = time.perf_counter() - t1 - info["t_load_s"]
+        return mod, launches
+
+    def _verdict(self, cmp: dict, info: dict) -> Observation | None:
+        """Verification outcome (None = passed) of an on-device comparison."""
+        info["verify"] = cmp
+        rel = cmp["max_abs_err"] / cmp["max_abs_ref"] if cmp["max_abs_ref"] > 0 else cmp["max_abs_err"]
+        info["verify_rel_err"] = rel
+        abs_tol = getattr(self.problem, "abs_tol", None)
+        bad = (cmp["max_abs_err"] > abs_tol) if abs_tol is not None else (rel > self.problem.rtol)
+        if cmp["n_nonfinite"] or bad:
+            self.stats["verify_failed"] += 1
+            return Observation(
+                Status.RUNTIME_FAILED,
+                detail=(f"verification failed: max_abs_err={cmp['max_abs_err']:.3e} "
+                        f"max_abs_ref={cmp['max_abs_ref']:.3e} "
+                        f"nonfinite={cmp['n_nonfinite']} bad={cmp['n_bad']}"),
+            )
+        return None
+
+    def execute_many(self, configs, protocol: MeasurementProtocol, on_config=None):
+        """Measure ``configs`` in order; yields (config, Observation) in order.
+
+        Same protocol and measurement as :meth:`execute` (per-run CUDA
+        events around each run on the one stream, L2 flush outside them,
+        on-device verification), but pipelined two deep through the C ABI's
+        submission slots (tsg_submit_timed / tsg_collect): configuration
+        i+1 is compiled-waited, loaded, set up and ENQUEUED before the host
+        waits for configuration i, so the device never idles between
+        configurations.  Compilation prefetch and module preload run ahead
+        as in :meth:`execute`.  ``on_config(i)`` (optional) is called before
+        each configuration is prepared (bench: clock sampling).
+        """
+        configs = list(configs)
+
+        def finish(p):
+            config, key, mod, n_launch, info, sl, t0 = p
+            try:
+                rc, times, lt, cmp = self.dev.collect(sl, protocol.benchmark_runs, n_launch, protocol.timeout_ms)
+                info["t_run_s"] = time.perf_counter() - info.pop("_t_submit")
+                if rc != rt.OK:
+                    return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(times))
+                info["launch_ms"] = lt
+                info["n_launches"] = n_launch
+                if self.verify:
+                    bad = self._verdict(cmp, info)
+                    if bad is not None:
+                        return bad
+                self.stats["executed"] += 1
+                self.stats["gpu_ms"] += sum(times)
+                return Observation(Status.OK, times_ms=tuple(times), time_ms=aggregate_times(protocol, times))
+            finally:
+                self._retire(mod, key, self.problem.kernel_name)
+                info["t_total_s"] = time.perf_counter() - t0
+                self.extras[key] = info
+
+        try:
+            yield from self._pipeline(configs, protocol, on_config, finish)
+        finally:
+            # a consumer that stops early leaves no slot in flight
+            for p in self._slots_inflight:
+                finish(p)
+            self._slots_inflight = []
+
+    def _pipeline(self, configs, protocol, on_config, finish):
+        slot = 0
+        self._slots_inflight = []
+        for i, config in enumerate(configs):
+            if i % 4 == 0:
+                self.prefetch(configs[i:])
+            self.preload(configs[i + 1:])
+            if on_config is not None:
+                on_config(i)
+            key = config_key(config)
+            info: dict = {"pipelined": True}
+            t0 = time.perf_counter()
+            immediate = None
+            if self.dev.poisoned:
+                immediate = Observation(Status.RUNTIME_FAILED, detail="device context poisoned by an earlier fault")
+            else:
+                prep = self._prepare(config, info)
+                if isinstance(prep, Observation):
+                    immediate = prep
+                else:
+                    mod, launches = prep
+                    info["_t_submit"] = time.perf_counter()
+                    rc, err = self.dev.submit_timed(slot, launches, protocol.warmup_runs, protocol.benchmark_runs,
+                                                    protocol.flush_l2, self.out if self.verify else None,
+                                                    self.n_out, self.answer_buf if self.verify else None,
+                                                    self.problem.rtol, self.problem.atol)
+                    if rc != rt.OK:
+                        info.pop("_t_submit", None)
+                        self._retire(mod, key, self.problem.kernel_name)
+                        self.extras[key] = info
+                        immediate = Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=err)
+            # configuration i-1 finishes while i (if enqueued) runs
+            if self._slots_inflight:
+                p = self._slots_inflight.pop()
+                yield p[0], finish(p)
+            if immediate is not None:
+                self.extras.setdefault(key, info)
+                yield config, immediate
+            else:
+                self._slots_inflight.append((config, key, mod, len(launches), info, slot, t0))
+                slot ^= 1
+        if self._slots_inflight:
+            p = self._slots_inflight.pop()
+            yield p[0], finish(p)
 
     def run_output(self, config) -> tuple:
         """Run one configuration once and return (Observation-like status, host output)."""

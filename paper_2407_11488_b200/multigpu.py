@@ -27,7 +27,7 @@ from __future__ import annotations
 import os
 from dataclasses import dataclass
 
-from .measure import BackendDescriptor, MeasurementProtocol, Observation, run_config
+from .measure import BackendDescriptor, MeasurementProtocol, Observation, run_configs
 from .paramspace import config_key
 from .store import ResultLog, TuningCache
 from .strategies import StrategyResult, result_to_cache
@@ -88,17 +88,16 @@ def sharded_sweep(space, configs: list, backend: BackendDescriptor, protocol: Me
             break
         n_chunks += 1
         lo, hi = rng
-        if backend.kind == "cuda":
-            backend.target.prefetch(configs[lo:hi])
-        for idx in range(lo, hi):
-            c = configs[idx]
+        todo = [configs[idx] for idx in range(lo, hi) if config_key(configs[idx]) not in done]
+        fresh = {}
+        for c, obs in run_configs(space, backend, protocol, todo):  # cuda: pipelined
             key = config_key(c)
-            obs = done.get(key)
-            if obs is None:
-                obs = run_config(space, backend, protocol, c)
-                if log:
-                    log.append(key, obs)
-            mine.append((idx, key, obs))
+            fresh[key] = obs
+            if log:
+                log.append(key, obs)
+        for idx in range(lo, hi):
+            key = config_key(configs[idx])
+            mine.append((idx, key, done.get(key) or fresh[key]))
     stats = ShardStats(rank, len(mine), n_chunks, time.perf_counter() - t0)
     if log:
         log.close()

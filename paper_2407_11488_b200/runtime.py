@@ -96,6 +96,12 @@ SIGNATURES = {
     "tsg_compare_f32": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_size_t, C.c_double,
                                   C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                   C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    "tsg_submit_timed": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(LaunchT), C.c_int, C.c_int, C.c_int,
+                                   C.c_int, C.c_uint64, C.c_size_t, C.c_uint64, C.c_double, C.c_double]),
+    "tsg_collect": (C.c_int, [C.c_void_p, C.c_int, C.c_double, C.POINTER(C.c_float), C.POINTER(C.c_float),
+                              C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_uint64),
+                              C.POINTER(C.c_uint64)]),
+    "tsg_slot_reset": (C.c_int, [C.c_void_p, C.c_int]),
 }
 
 _lib = None
@@ -388,6 +394,38 @@ class Device:
                 self.poisoned = True
             return rc, last_error()
         return OK, [float(t) for t in times]
+
+    def submit_timed(self, slot: int, launches: list, warmup: int, runs: int, flush_l2: bool,
+                     out: "Buffer | None", n_out: int, ref: "Buffer | None", rtol: float = 0.0,
+                     atol: float = 0.0) -> tuple:
+        """Enqueue one configuration's protocol into ``slot`` without waiting
+        (tsg_submit_timed); returns (status_code, error text)."""
+        arr = (LaunchT * len(launches))(*[l.to_struct() for l in launches])
+        rc = self.lib.tsg_submit_timed(self.ctx, int(slot), arr, len(launches), int(warmup), int(runs),
+                                       1 if flush_l2 else 0, out.ptr if out is not None else 0, int(n_out),
+                                       ref.ptr if ref is not None else 0, float(rtol), float(atol))
+        if rc != OK:
+            err = last_error()
+            if rc in (ERR_RUNTIME, ERR_TIMEOUT):
+                self.poisoned = True
+            self.lib.tsg_slot_reset(self.ctx, int(slot))
+            return rc, err
+        return OK, ""
+
+    def collect(self, slot: int, runs: int, n_launch: int, timeout_ms: float = 60000.0) -> tuple:
+        """Wait for ``slot``; returns (status_code, times | error, per-launch times, compare dict)."""
+        times = (C.c_float * runs)()
+        lt = (C.c_float * n_launch)()
+        e, r = C.c_double(), C.c_double()
+        bad, nf = C.c_uint64(), C.c_uint64()
+        rc = self.lib.tsg_collect(self.ctx, int(slot), float(timeout_ms), times, lt, int(n_launch), C.byref(e),
+                                  C.byref(r), C.byref(bad), C.byref(nf))
+        if rc != OK:
+            if rc in (ERR_RUNTIME, ERR_TIMEOUT):
+                self.poisoned = True
+            return rc, last_error(), None, None
+        cmp = dict(max_abs_err=e.value, max_abs_ref=r.value, n_bad=int(bad.value), n_nonfinite=int(nf.value))
+        return OK, [float(t) for t in times], [float(x) for x in lt], cmp
 
     def last_launch_times(self, n: int) -> list:
         t = (C.c_float * n)()

@@ -25,7 +25,7 @@ import random
 from dataclasses import dataclass
 
 from .errors import ProtocolError
-from .measure import BackendDescriptor, MeasurementProtocol, Observation, run_config
+from .measure import BackendDescriptor, MeasurementProtocol, Observation, pipelined, run_config, run_configs
 from .paramspace import Config, NeighborScheme, SearchSpaceSpec, config_key
 from .store import TuningCache
 
@@ -84,6 +84,18 @@ class Runner:
             return hit
         return self.record(config, run_config(self.space, self.backend, self.protocol, config))
 
+    def evaluate_many(self, configs) -> None:
+        """Evaluate a list fixed in advance, in order (memoised; the cuda
+        backend pipelines it -- same trace as evaluating one by one)."""
+        todo, keys = [], set()
+        for c in configs:
+            k = config_key(c)
+            if k not in self.seen and k not in keys:
+                keys.add(k)
+                todo.append(c)
+        for c, obs in run_configs(self.space, self.backend, self.protocol, todo):
+            self.record(c, obs)
+
     def result(self, notes=(), segments=()) -> StrategyResult:
         notes = tuple(notes)
         if self.best is None:
@@ -131,10 +143,13 @@ def brute_force(space: SearchSpaceSpec, backend: BackendDescriptor,
     """
     runner = Runner(space, backend, protocol)
     todo = list(space.enumerate_configs()) if configs is None else list(configs)
-    for i, config in enumerate(todo):
-        if i % 8 == 0:
-            _window(runner, todo, i)
-        runner.evaluate(config)
+    if pipelined(backend):
+        runner.evaluate_many(todo)  # pipelined, same order
+    else:
+        for i, config in enumerate(todo):
+            if i % 8 == 0:
+                _window(runner, todo, i)
+            runner.evaluate(config)
     result = runner.result()
     return result, result_to_cache(space, result, default_device_name(backend, device_name),
                                    metadata)
@@ -185,10 +200,13 @@ def random_search(space: SearchSpaceSpec, backend: BackendDescriptor,
     """Uniform sampling without replacement (seeded, replayable)."""
     order, notes = random_sample_sequence(space, budget, seed)
     runner = Runner(space, backend, protocol)
-    for i, config in enumerate(order):
-        if i % 8 == 0:
-            _window(runner, order, i)
-        runner.evaluate(config)
+    if pipelined(backend):
+        runner.evaluate_many(order)  # the order is timing-independent: pipelined
+    else:
+        for i, config in enumerate(order):
+            if i % 8 == 0:
+                _window(runner, order, i)
+            runner.evaluate(config)
     return runner.result(notes=notes)
 
 
