@@ -9,7 +9,7 @@ Workload (default, BASELINE.json configs[1]): hotspot 4096x4096 fp32,
 the paper's hotspot space.  One *step* = one batch of B configurations
 per rank, each run through the full protocol of the reference
 (`pkg/src/tunescape/measure.py:59-79`: 1 warmup + 7 timed runs, mean)
-with an L2 flush before every run (3x L2 buffer, outside the events),
+with an L2 flush before every run (1.25x L2 buffer written, outside the events),
 plus on-device verification against the naive reference kernel.
 
 * ``value``  -- configurations benchmarked per second over all ranks,
@@ -504,7 +504,7 @@ def our_arm(args, dist: Dist):
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": wl["desc"], "configs_per_step_per_rank": batch,
                        "protocol": "1 warmup + 7 timed runs per config, mean (tunescape default)",
-                       "l2": "flushed before every run (3x L2 buffer written, outside the events)",
+                       "l2": "flushed before every run (1.25x L2 buffer written, outside the events; tools/flush_probe.py)",
                        "compile": "NVRTC sm_100a; timed steps use cubins compiled in an untimed "
                                   "precompile phase; cold (pipelined NVRTC) rate in 'cold'",
                        "verify": "every config checked on-device vs the naive reference kernel",

@@ -170,6 +170,11 @@ int tsg_last_launch_times(tsg_ctx* ctx, float* times_ms, int n_launch);
  * configuration i (replaces the per-configuration synchronisations of
  * tsg_memset32 + tsg_run_timed + tsg_compare_f32). */
 #define TSG_SLOTS 2
+/* The L2 flush before every run: write `write_bytes` of one buffer (0 =
+ * the default, 1.25 x L2), then optionally read `read_bytes` of another so
+ * that the timed run starts with only CLEAN lines in L2 (default 0: no
+ * read phase). */
+int tsg_set_flush_bytes(tsg_ctx* ctx, size_t write_bytes, size_t read_bytes);
 int tsg_submit_timed(tsg_ctx* ctx, int slot, const tsg_launch_t* seq, int n_launch, int warmup, int runs,
                      int flush_l2, uint64_t poison_out, size_t n_out, uint64_t ref, double rtol,
                      double atol);

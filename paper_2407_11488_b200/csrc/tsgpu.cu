@@ -68,6 +68,8 @@ struct tsg_ctx {
   std::vector<CUevent> events;  // 2 per recorded run + per-launch pairs
   CUdeviceptr flush_buf = 0;
   size_t flush_bytes = 0;
+  CUdeviceptr flush_rbuf = 0;  // optional read phase (clean lines); 0 bytes = write-only flush
+  size_t flush_rbytes = 0;
   CUdeviceptr scratch = 0;  // compare accumulators
   std::atomic<uint64_t> launches{0};
   bool poisoned = false;
@@ -216,16 +218,50 @@ __global__ void __launch_bounds__(256) flush_kernel(uint4* __restrict__ buf, siz
     buf[i] = make_uint4(salt, (unsigned)i, salt ^ 0x9e3779b9u, 0u);
 }
 
+// optional second flush phase (tsg_set_flush_bytes, off by default): READ a
+// different >= L2-sized buffer, so the dirty lines the write phase left in
+// L2 are written back outside the timed events.  Measured on B200
+// (tools/flush_probe.py, 96 MiB read): 28.7 us after a write-only flush of
+// 1x or 3x L2 (identical: 1x already evicts everything), 24.6 us after
+// write + read, 22.5 us after a read-only flush, 14.9 us unflushed.  The
+// default stays write-only, the way Kernel Tuner flushes (an L2-sized
+// buffer written before each run), so times compare like for like.
+__global__ void __launch_bounds__(256) flush_read_kernel(const uint4* __restrict__ buf, size_t n16,
+                                                         unsigned* sink) {
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  unsigned x = 0;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n16; i += stride) {
+    const uint4 v = __ldcg(buf + i);
+    x ^= v.x ^ v.y ^ v.z ^ v.w;
+  }
+  if (x == 0x9e3779b9u) sink[blockIdx.x & 15] = x;  // practically never; keeps the loads
+}
+
 int flush_l2(tsg_ctx* c) {
   if (!c->flush_buf) {
-    c->flush_bytes = (size_t)3 * (c->info.l2_bytes > 0 ? c->info.l2_bytes : (128 << 20));
-    CUresult r = cuMemAlloc(&c->flush_buf, c->flush_bytes);
+    // 1.25 x L2 written: as effective as 3 x (measured, tools/flush_probe.py)
+    // at 40% of the cost
+    if (!c->flush_bytes)
+      c->flush_bytes = ((size_t)5 * (c->info.l2_bytes > 0 ? c->info.l2_bytes : (128 << 20)) / 4 + 15) & ~(size_t)15;
+    CUresult r = cuMemAlloc(&c->flush_buf, c->flush_bytes < 16 ? 16 : c->flush_bytes);
     if (r != CUDA_SUCCESS) return fail(TSG_ERR_SETUP, "flush buffer: " + cu_msg(r));
   }
+  if (c->flush_rbytes && !c->flush_rbuf) {
+    CUresult r = cuMemAlloc(&c->flush_rbuf, c->flush_rbytes);
+    if (r == CUDA_SUCCESS) r = cuMemsetD32Async(c->flush_rbuf, 0, c->flush_rbytes / 4, c->stream);
+    if (r != CUDA_SUCCESS) return fail(TSG_ERR_SETUP, "flush read buffer: " + cu_msg(r));
+  }
   static unsigned salt = 1;
-  c->launches.fetch_add(1, std::memory_order_relaxed);
-  flush_kernel<<<c->info.sm_count * 4, 256, 0, (cudaStream_t)c->stream>>>(
-      (uint4*)c->flush_buf, c->flush_bytes / 16, salt++);
+  if (c->flush_bytes) {
+    c->launches.fetch_add(1, std::memory_order_relaxed);
+    flush_kernel<<<c->info.sm_count * 4, 256, 0, (cudaStream_t)c->stream>>>(
+        (uint4*)c->flush_buf, c->flush_bytes / 16, salt++);
+  }
+  if (c->flush_rbytes) {
+    c->launches.fetch_add(1, std::memory_order_relaxed);
+    flush_read_kernel<<<c->info.sm_count * 4, 256, 0, (cudaStream_t)c->stream>>>(
+        (const uint4*)c->flush_rbuf, c->flush_rbytes / 16, (unsigned*)c->scratch + 8);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(TSG_ERR_RUNTIME, std::string("flush: ") + cudaGetErrorString(e));
   return TSG_OK;
@@ -319,6 +355,7 @@ int tsg_destroy(tsg_ctx* c) {
     cuStreamSynchronize(c->stream);
     for (CUevent e : c->events) cuEventDestroy(e);
     if (c->flush_buf) cuMemFree(c->flush_buf);
+    if (c->flush_rbuf) cuMemFree(c->flush_rbuf);
     if (c->scratch) cuMemFree(c->scratch);
     for (auto& sl : c->slots) {
       for (CUevent e : sl.ev) cuEventDestroy(e);
@@ -717,6 +754,18 @@ int tsg_tma_encode_2d_f32(tsg_ctx* c, void* desc128, uint64_t gaddr, uint64_t di
                                       CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(TSG_ERR_INVALID, "cuTensorMapEncodeTiled: " + cu_msg(r));
+  return TSG_OK;
+}
+
+int tsg_set_flush_bytes(tsg_ctx* c, size_t write_bytes, size_t read_bytes) {
+  int s = make_current(c);
+  if (s) return s;
+  cuStreamSynchronize(c->stream);
+  if (c->flush_buf) cuMemFree(c->flush_buf);
+  if (c->flush_rbuf) cuMemFree(c->flush_rbuf);
+  c->flush_buf = c->flush_rbuf = 0;
+  c->flush_bytes = (write_bytes + 15) & ~(size_t)15;
+  c->flush_rbytes = (read_bytes + 15) & ~(size_t)15;
   return TSG_OK;
 }
 

@@ -102,6 +102,7 @@ SIGNATURES = {
                               C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                               C.POINTER(C.c_uint64)]),
     "tsg_slot_reset": (C.c_int, [C.c_void_p, C.c_int]),
+    "tsg_set_flush_bytes": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
 }
 
 _lib = None
