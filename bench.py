@@ -493,7 +493,8 @@ def our_arm(args, dist: Dist):
             rows.append({"config": list(c), "status": o.status.value, "time_ms": o.time_ms,
                          "regs": info.get("regs"), "smem": info.get("smem_bytes"),
                          "launch_ms": info.get("launch_ms"),
-                         "host_s": {k: round(v, 6) for k, v in info.items() if k.startswith("t_")}})
+                         "host_s": {k: round(v, 6) for k, v in info.items()
+                                    if k.startswith("t_") or k == "compile_wait_s"}})
         Path(args.dump).write_text(json.dumps({"workload": args.workload, "rows": rows}))
     all_best = dist.gather_obj(best)
     if dist.rank == 0:

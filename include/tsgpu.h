@@ -166,10 +166,10 @@ int tsg_last_launch_times(tsg_ctx* ctx, float* times_ms, int n_launch);
  * returns the per-run times, the last run's per-launch times (n_launch
  * floats, may be NULL) and the comparison.  A slot must be collected
  * before it is submitted again; tsg_slot_reset drops a failed submission.
- * Two slots let the host prepare configuration i+1 while the device runs
- * configuration i (replaces the per-configuration synchronisations of
+ * Several slots let the host prepare configuration i+1 while the device
+ * runs configurations i, i-1, ... (replaces the per-configuration synchronisations of
  * tsg_memset32 + tsg_run_timed + tsg_compare_f32). */
-#define TSG_SLOTS 2
+#define TSG_SLOTS 8
 /* The L2 flush before every run: write `write_bytes` of one buffer (0 =
  * the default, 1.25 x L2), then optionally read `read_bytes` of another so
  * that the timed run starts with only CLEAN lines in L2 (default 0: no

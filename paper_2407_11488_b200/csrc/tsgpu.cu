@@ -75,6 +75,7 @@ struct tsg_ctx {
   bool poisoned = false;
   std::vector<float> last_launch_ms;
   CUevent marks[16] = {};
+  bool lmem_to_max = false;  // CU_CTX_LMEM_RESIZE_TO_MAX applied
   // pipelined submission slots (tsg_submit_timed / tsg_collect)
   struct Slot {
     std::vector<CUevent> ev;  // [2*total run brackets][n+1 launch marks][done]
@@ -314,6 +315,22 @@ int tsg_init(int device, tsg_ctx** out) {
     return fail(TSG_ERR_SETUP, "cuDevicePrimaryCtxRetain: " + cu_msg(r));
   }
   cuCtxSetCurrent(c->cu);
+  // Keep local memory at its high-water mark: by default the driver shrinks
+  // it again after a kernel that needed more, so every launch of a spilling
+  // configuration re-grows it (device-wide sync + reallocation, measured as
+  // 25-60 ms stalls per such configuration in a sweep).  cuCtxSetFlags is a
+  // CUDA 12.1 entry point, looked up optionally; TSG_LMEM_RESIZE_TO_MAX=0
+  // keeps the driver default (A/B measurements).
+  {
+    const char* env = getenv("TSG_LMEM_RESIZE_TO_MAX");
+    typedef CUresult (*GetFlagsFn)(unsigned*);
+    typedef CUresult (*SetFlagsFn)(unsigned);
+    auto getf = (GetFlagsFn)dlsym(RTLD_DEFAULT, "cuCtxGetFlags");
+    auto setf = (SetFlagsFn)dlsym(RTLD_DEFAULT, "cuCtxSetFlags");
+    unsigned flags = 0;
+    if (!(env && env[0] == '0') && getf && setf && getf(&flags) == CUDA_SUCCESS)
+      c->lmem_to_max = setf(flags | CU_CTX_LMEM_RESIZE_TO_MAX) == CUDA_SUCCESS;
+  }
   cudaSetDevice(device);  // runtime API shares the primary context
   if ((r = cuStreamCreate(&c->stream, CU_STREAM_NON_BLOCKING)) != CUDA_SUCCESS) {
     cuDevicePrimaryCtxRelease(c->dev);

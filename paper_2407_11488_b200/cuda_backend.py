@@ -157,6 +157,7 @@ class CudaTarget:
         self.prefetch_depth = prefetch_depth or 4 * self.compiler.pool._max_workers
         self.stats = {"executed": 0, "gpu_ms": 0.0, "verify_failed": 0}
         self._slots_inflight: list = []  # execute_many: enqueued, not yet collected
+        self.pipeline_depth = 4          # configurations enqueued at once (<= rt.SLOTS)
 
     # -- answer ------------------------------------------------------------------
     def _load(self, image: bytes):
@@ -368,13 +369,15 @@ class CudaTarget:
 
         Same protocol and measurement as :meth:`execute` (per-run CUDA
         events around each run on the one stream, L2 flush outside them,
-        on-device verification), but pipelined two deep through the C ABI's
-        submission slots (tsg_submit_timed / tsg_collect): configuration
-        i+1 is compiled-waited, loaded, set up and ENQUEUED before the host
-        waits for configuration i, so the device never idles between
-        configurations.  Compilation prefetch and module preload run ahead
-        as in :meth:`execute`.  ``on_config(i)`` (optional) is called before
-        each configuration is prepared (bench: clock sampling).
+        on-device verification), but pipelined through the C ABI's
+        submission slots (tsg_submit_timed / tsg_collect): up to
+        ``pipeline_depth`` configurations are enqueued at once, and
+        configuration i+1 is compile-waited, loaded, set up and ENQUEUED
+        before the host waits for the oldest one, so the device never idles
+        between configurations.  Compilation prefetch and module preload
+        run ahead as in :meth:`execute`.  ``on_config(i)`` (optional) is
+        called before each configuration is prepared (bench: clock
+        sampling).
         """
         configs = list(configs)
 
@@ -382,7 +385,9 @@ class CudaTarget:
             config, key, mod, n_launch, info, sl, t0 = p
             try:
                 rc, times, lt, cmp = self.dev.collect(sl, protocol.benchmark_runs, n_launch, protocol.timeout_ms)
-                info["t_run_s"] = time.perf_counter() - info.pop("_t_submit")
+                info["t_run_s"] = time.perf_counter() - info["_t_submit"]
+                info["t_abs_submit"] = info.pop("_t_submit")  # host timeline (bench --dump)
+                info["t_abs_collected"] = time.perf_counter()
                 if rc != rt.OK:
                     return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(times))
                 info["launch_ms"] = lt
@@ -404,21 +409,42 @@ class CudaTarget:
         finally:
             # a consumer that stops early leaves no slot in flight
             for p in self._slots_inflight:
-                finish(p)
+                if p[0] == "pending":
+                    finish(p[2])
             self._slots_inflight = []
 
     def _pipeline(self, configs, protocol, on_config, finish):
-        slot = 0
-        self._slots_inflight = []
+        # FIFO of ("pending", config, state) / ("done", config, Observation):
+        # results leave in input order; up to pipeline_depth configurations
+        # are enqueued on the device at once (absorbs host hiccups longer
+        # than one configuration's device time)
+        fifo = self._slots_inflight = []
+        free = list(range(rt.SLOTS))
+        depth = max(1, min(self.pipeline_depth, rt.SLOTS))
+
+        def n_pending():
+            return sum(1 for e in fifo if e[0] == "pending")
+
+        def drain(limit):
+            while fifo and (fifo[0][0] == "done" or n_pending() > limit):
+                kind, config, x = fifo.pop(0)
+                if kind == "pending":
+                    free.append(x[5])
+                    yield config, finish(x)
+                else:
+                    yield config, x
+
         for i, config in enumerate(configs):
             if i % 4 == 0:
                 self.prefetch(configs[i:])
             self.preload(configs[i + 1:])
             if on_config is not None:
                 on_config(i)
+            yield from drain(depth - 1)  # a slot is free
             key = config_key(config)
             info: dict = {"pipelined": True}
             t0 = time.perf_counter()
+            info["t_abs_prepare"] = t0
             immediate = None
             if self.dev.poisoned:
                 immediate = Observation(Status.RUNTIME_FAILED, detail="device context poisoned by an earlier fault")
@@ -428,29 +454,25 @@ class CudaTarget:
                     immediate = prep
                 else:
                     mod, launches = prep
+                    slot = free.pop(0)
                     info["_t_submit"] = time.perf_counter()
                     rc, err = self.dev.submit_timed(slot, launches, protocol.warmup_runs, protocol.benchmark_runs,
                                                     protocol.flush_l2, self.out if self.verify else None,
                                                     self.n_out, self.answer_buf if self.verify else None,
                                                     self.problem.rtol, self.problem.atol)
                     if rc != rt.OK:
+                        free.append(slot)
                         info.pop("_t_submit", None)
                         self._retire(mod, key, self.problem.kernel_name)
                         self.extras[key] = info
                         immediate = Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=err)
-            # configuration i-1 finishes while i (if enqueued) runs
-            if self._slots_inflight:
-                p = self._slots_inflight.pop()
-                yield p[0], finish(p)
+                    else:
+                        fifo.append(("pending", config, (config, key, mod, len(launches), info, slot, t0)))
             if immediate is not None:
                 self.extras.setdefault(key, info)
-                yield config, immediate
-            else:
-                self._slots_inflight.append((config, key, mod, len(launches), info, slot, t0))
-                slot ^= 1
-        if self._slots_inflight:
-            p = self._slots_inflight.pop()
-            yield p[0], finish(p)
+                fifo.append(("done", config, immediate))
+            yield from drain(depth - 1)
+        yield from drain(-1)
 
     def run_output(self, config) -> tuple:
         """Run one configuration once and return (Observation-like status, host output)."""

@@ -36,8 +36,11 @@ def test_pipelined_matches_sequential(device):
     tgt = CudaTarget(prob, device=device, answer=want)
     try:
         seq = {c: tgt.execute(c, PROTO) for c in configs}
-        pip = list(tgt.execute_many(configs, PROTO))
-        assert [c for c, _ in pip] == configs
+        for depth in (1, 2, 3, 4):
+            tgt.pipeline_depth = depth
+            pip = list(tgt.execute_many(configs, PROTO))
+            assert [c for c, _ in pip] == configs
+            assert [o.status for _, o in pip] == [seq[c].status for c in configs]
         for c, o in pip:
             assert o.status is seq[c].status, (c, o, seq[c])
             if o.ok:

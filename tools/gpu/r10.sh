@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+for i in 1 2; do
+timeout 600 python bench.py --no-e2e --dump gpurun_out/dump_$i.json > gpurun_out/bench_$i.json 2> gpurun_out/bench_$i.err
+done
+TSG_LMEM_RESIZE_TO_MAX=0 timeout 600 python bench.py --no-e2e --dump gpurun_out/dump_3.json > gpurun_out/bench_3.json 2> gpurun_out/bench_3.err
