@@ -19,3 +19,5 @@ for w in hotspot convolution gemm dedispersion; do
   tag=$(echo $cfg | tr ',' '-')
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:${w}_kernel -s 1 -c 1 -o gpurun_out/prof_best_${w}_${tag} -f python tools/run_config.py $w $cfg --runs 1 > gpurun_out/ncu_best_$w.log 2>&1
 done
+# staged generic dedispersion (DD_STG) evidence
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:dedispersion_kernel -s 1 -c 1 -o gpurun_out/prof_dd_staged_16-64-4-3-1-0 -f python tools/run_config.py dedispersion 16,64,4,3,1,0 --runs 1 > gpurun_out/ncu_dd_staged.log 2>&1

@@ -1,6 +1,6 @@
 """Collect per-launch DRAM traffic from the committed ncu summaries.
 
-    python tools/traffic_table.py [profiles/round1] > profiles/traffic.json
+    python tools/traffic_table.py [profiles/round1 profiles/round1/final ...] > profiles/traffic.json
 
 Each ``ncu_<kernel>[_<mode>]_<c-o-n-f-i-g>.md`` summary (tools/ncu_summary.py
 output of one ``ncu --set full`` capture) gives dram__bytes_read.sum +
@@ -17,10 +17,11 @@ from pathlib import Path
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
 
-def main(d: str = "profiles/round1") -> None:
+def main(*dirs: str) -> None:
     out: dict = {}
-    for f in sorted(Path(d).glob("ncu_*.md")):
-        m = re.match(r"ncu_([a-z_]+?)(?:_(?:stream|window))?_([0-9-]+)\.md$", f.name)
+    files = [f for d in (dirs or ("profiles/round1", "profiles/round1/final")) for f in sorted(Path(d).glob("ncu_*.md"))]
+    for f in files:  # directories in order: later captures win
+        m = re.match(r"ncu_([a-z_]+?)(?:_(?:stream|window|staged))?_([0-9-]+)\.md$", f.name)
         if not m:
             continue
         kernel, cfg = m.group(1), m.group(2).replace("-", ",")
