@@ -303,17 +303,26 @@ class Hotspot(Problem):
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
                     UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"],
                     HS_STREAM=(self.stream_geometry(cfg) or {}).get("kind", 0),
-                    HS_REM=self.iterations % cfg["temporal_tiling_factor"], HS_NR=self.stream_nr(cfg["temporal_tiling_factor"]))
+                    HS_REM=self.iterations % cfg["temporal_tiling_factor"],
+                    HS_NR=(self.stream_geometry(cfg) or {}).get("nr", 8))
 
     # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
-    # cp.async input ring depth (rows): deeper for T >= 6 (measured on B200:
-    # T=8 0.238 -> 0.205 ms with 16 rows; T <= 5 unchanged or slightly slower);
+    # cp.async input ring depth (rows), measured on B200:
+    # * register rings, two rows per iteration: 16 rows for T >= 6 (T=8
+    #   0.238 -> 0.205 ms), 8 below;
+    # * shared-memory rings (kind 2) and register rings with one row per
+    #   iteration at T >= 6: 4 rows -- the smaller input (and power) ring
+    #   raises occupancy; 24-configuration samples: kind 2 1.16x geomean
+    #   over 16 rows (never slower), one-row register rings 1.03x
+    #   (tools/gpu/hs_nr2.sh).
     # TSG_HS_NR forces one value for experiments
     STREAM_NR_ENV = os.environ.get("TSG_HS_NR")
 
-    def stream_nr(self, t: int) -> int:
+    def stream_nr(self, t: int, kind: int = 1, unroll: int = 2) -> int:
         if self.STREAM_NR_ENV:
             return int(self.STREAM_NR_ENV)
+        if kind == 2 or (unroll == 1 and t >= 6):
+            return 4
         return 16 if t >= 6 else 8
     STREAM_SMEM_MAX = 200 * 1024
     STREAM_REG_BASE = 48     # addresses, masks, coefficients, temporaries
@@ -353,7 +362,7 @@ class Hotspot(Problem):
         uw = ((sw - ta - t) // 4) * 4
         if uw < 4:
             return None
-        nr = self.stream_nr(t)
+        nr = self.stream_nr(t, kind, cfg["loop_unroll_factor_t"])
         pr = (16 if t + nr + 2 <= 16 else (32 if t + nr + 2 <= 32 else 64)) if shp else 0
         wpb = nthreads // 32
         warp_floats = sw * (nr + pr + (3 * t if kind == 2 else 0))
@@ -372,7 +381,7 @@ class Hotspot(Problem):
         segh, segh0, nsegs = self._segments(nsegs)
         return dict(sw=sw, ta=ta, uw=uw, segh=segh, segh0=segh0, wpb=wpb, smem=smem, nstrips=nstrips,
                     nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb), blocks_per_sm=blocks_per_sm,
-                    kind=kind)
+                    kind=kind, nr=nr)
 
     def _smem_ring_regs(self, t: int, tsx: int) -> int:
         """Register estimate of the smem-ring stream kernel (ptxas hoists
