@@ -181,6 +181,10 @@ int tsg_submit_timed(tsg_ctx* ctx, int slot, const tsg_launch_t* seq, int n_laun
 int tsg_collect(tsg_ctx* ctx, int slot, double timeout_ms, float* times_ms, float* launch_ms, int n_launch,
                 double* max_abs_err, double* max_abs_ref, uint64_t* n_bad, uint64_t* n_nonfinite);
 int tsg_slot_reset(tsg_ctx* ctx, int slot);
+/* Device timeline of a collected slot (until its next submission): start
+ * and end of the whole submission in ms since the context's first
+ * submission, and the warm-up run's duration (sweep-efficiency analysis). */
+int tsg_slot_timeline(tsg_ctx* ctx, int slot, double* start_ms, double* end_ms, float* warmup_ms);
 
 /* TMA: encode a 2-D fp32 tensor map (CUtensorMap, 128 bytes written to
  * `desc128`) for `cp.async.bulk.tensor` in kernels that take it as a

@@ -76,6 +76,7 @@ struct tsg_ctx {
   std::vector<float> last_launch_ms;
   CUevent marks[16] = {};
   bool lmem_to_max = false;  // CU_CTX_LMEM_RESIZE_TO_MAX applied
+  CUevent epoch = nullptr;   // device-timeline origin of the submission slots
   // pipelined submission slots (tsg_submit_timed / tsg_collect)
   struct Slot {
     std::vector<CUevent> ev;  // [2*total run brackets][n+1 launch marks][done]
@@ -374,6 +375,7 @@ int tsg_destroy(tsg_ctx* c) {
     if (c->flush_buf) cuMemFree(c->flush_buf);
     if (c->flush_rbuf) cuMemFree(c->flush_rbuf);
     if (c->scratch) cuMemFree(c->scratch);
+    if (c->epoch) cuEventDestroy(c->epoch);
     for (auto& sl : c->slots) {
       for (CUevent e : sl.ev) cuEventDestroy(e);
       if (sl.scratch) cuMemFree(sl.scratch);
@@ -654,7 +656,7 @@ int tsg_submit_timed(tsg_ctx* c, int slot, const tsg_launch_t* seq, int n, int w
   auto& sl = c->slots[slot];
   if (sl.active) return fail(TSG_ERR_ARG, "slot still in flight (collect it first)");
   const int total = warmup + runs;
-  const size_t need = 2 * (size_t)total + n + 2;
+  const size_t need = 2 * (size_t)total + n + 3;  // + slot start + done
   while (sl.ev.size() < need) {
     CUevent e;
     CUresult r = cuEventCreate(&e, CU_EVENT_DEFAULT);
@@ -677,6 +679,12 @@ int tsg_submit_timed(tsg_ctx* c, int slot, const tsg_launch_t* seq, int n, int w
   CUevent* ev = sl.ev.data();
   CUevent* lev = ev + 2 * total;
   CUresult r;
+  if (!c->epoch) {
+    if ((r = cuEventCreate(&c->epoch, CU_EVENT_DEFAULT)) != CUDA_SUCCESS)
+      return fail(TSG_ERR_SETUP, "cuEventCreate: " + cu_msg(r));
+    cuEventRecord(c->epoch, c->stream);
+  }
+  cuEventRecord(ev[need - 2], c->stream);  // slot start (before the poison)
   if (poison_out && (r = cuMemsetD32Async((CUdeviceptr)poison_out, 0x7FC00000u, n_out, c->stream)) != CUDA_SUCCESS)
     return fail(TSG_ERR_RUNTIME, "poison: " + cu_msg(r));
   for (int k = 0; k < total; ++k) {
@@ -720,7 +728,7 @@ int tsg_collect(tsg_ctx* c, int slot, double timeout_ms, float* times_ms, float*
   sl.active = false;
   const int total = sl.warmup + sl.runs;
   CUevent* ev = sl.ev.data();
-  if ((s = wait_stream(c, ev[2 * (size_t)total + sl.n + 1], timeout_ms))) return s;
+  if ((s = wait_stream(c, ev[2 * (size_t)total + sl.n + 2], timeout_ms))) return s;
   for (int k = sl.warmup; k < total; ++k) cuEventElapsedTime(&times_ms[k - sl.warmup], ev[2 * k], ev[2 * k + 1]);
   CUevent* lev = ev + 2 * total;
   c->last_launch_ms.assign(sl.n, 0.f);
@@ -738,6 +746,26 @@ int tsg_collect(tsg_ctx* c, int slot, double timeout_ms, float* times_ms, float*
     if (n_bad) *n_bad = acc[2];
     if (n_nonfinite) *n_nonfinite = acc[3];
   }
+  return TSG_OK;
+}
+
+/* Device timeline of a collected slot (valid until the slot is submitted
+ * again): start / end of its whole submission in ms since the first
+ * submission on this context, and its warm-up run's duration. */
+int tsg_slot_timeline(tsg_ctx* c, int slot, double* start_ms, double* end_ms, float* warmup_ms) {
+  if (!c) return fail(TSG_ERR_ARG, "null context");
+  if (slot < 0 || slot >= TSG_SLOTS) return fail(TSG_ERR_ARG, "slot out of range");
+  auto& sl = c->slots[slot];
+  if (sl.active || !c->epoch || sl.ev.empty()) return fail(TSG_ERR_ARG, "slot not collected");
+  const size_t total = sl.warmup + sl.runs;
+  const size_t start = 2 * total + sl.n + 1, done = start + 1;
+  float a = 0.f, b = 0.f, w = 0.f;
+  cuEventElapsedTime(&a, c->epoch, sl.ev[start]);
+  cuEventElapsedTime(&b, c->epoch, sl.ev[done]);
+  if (sl.warmup > 0) cuEventElapsedTime(&w, sl.ev[0], sl.ev[1]);
+  if (start_ms) *start_ms = a;
+  if (end_ms) *end_ms = b;
+  if (warmup_ms) *warmup_ms = w;
   return TSG_OK;
 }
 

@@ -392,6 +392,9 @@ class CudaTarget:
                     return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=str(times))
                 info["launch_ms"] = lt
                 info["n_launches"] = n_launch
+                tl = self.dev.slot_timeline(sl)
+                if tl is not None:  # device timeline (ms): bench --dump
+                    info["t_dev_start_ms"], info["t_dev_end_ms"], info["t_dev_warmup_ms"] = tl
                 if self.verify:
                     bad = self._verdict(cmp, info)
                     if bad is not None:

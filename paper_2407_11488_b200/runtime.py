@@ -102,6 +102,8 @@ SIGNATURES = {
                               C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_uint64),
                               C.POINTER(C.c_uint64)]),
     "tsg_slot_reset": (C.c_int, [C.c_void_p, C.c_int]),
+    "tsg_slot_timeline": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                    C.POINTER(C.c_float)]),
     "tsg_set_flush_bytes": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
 }
 
@@ -429,6 +431,13 @@ class Device:
             return rc, last_error(), None, None
         cmp = dict(max_abs_err=e.value, max_abs_ref=r.value, n_bad=int(bad.value), n_nonfinite=int(nf.value))
         return OK, [float(t) for t in times], [float(x) for x in lt], cmp
+
+    def slot_timeline(self, slot: int) -> tuple:
+        """(start_ms, end_ms, warmup_ms) of a collected slot on the device timeline."""
+        a, b, w = C.c_double(), C.c_double(), C.c_float()
+        if self.lib.tsg_slot_timeline(self.ctx, int(slot), C.byref(a), C.byref(b), C.byref(w)) != OK:
+            return None
+        return a.value, b.value, w.value
 
     def last_launch_times(self, n: int) -> list:
         t = (C.c_float * n)()
