@@ -477,8 +477,11 @@ class CudaTarget:
             yield from drain(depth - 1)
         yield from drain(-1)
 
-    def run_output(self, config) -> tuple:
-        """Run one configuration once and return (Observation-like status, host output)."""
+    def run_output(self, config, out: np.ndarray | None = None) -> tuple:
+        """Run one configuration once and return (Observation-like status, host output).
+
+        ``out`` (optional): a float32 host array of ``output_count`` elements
+        to download into (e.g. page-locked memory: no staging copy)."""
         names = self.problem.space.param_names
         cfg = dict(zip(names, config))
         res = self._compiled(config_key(config), cfg)
@@ -497,7 +500,8 @@ class CudaTarget:
             rc, err = self.dev.run(self.problem.launches(cfg, kern, self.bufs))
             if rc != rt.OK:
                 return _RC_STATUS.get(rc, Status.RUNTIME_FAILED), err
-            out = np.empty(self.n_out, dtype=np.float32)
+            if out is None:
+                out = np.empty(self.n_out, dtype=np.float32)
             self.out.download(out)
             return Status.OK, out
         finally:
