@@ -436,6 +436,8 @@ def our_arm(args, dist: Dist):
     # -- e2e: public API with host buffers -----------------------------------------
     e2e = None
     if not args.no_e2e:
+        if os.environ.get("TSG_E2E_FLUSH_MODULES", "1") != "0":
+            target.flush_modules()  # unload the timed region's modules (untimed cleanup)
         host = {b.name: b.init for b in prob.buffers() if b.init is not None}
         pinned = {}
         for k, arr in host.items():

@@ -169,7 +169,7 @@ int tsg_last_launch_times(tsg_ctx* ctx, float* times_ms, int n_launch);
  * Several slots let the host prepare configuration i+1 while the device
  * runs configurations i, i-1, ... (replaces the per-configuration synchronisations of
  * tsg_memset32 + tsg_run_timed + tsg_compare_f32). */
-#define TSG_SLOTS 8
+#define TSG_SLOTS 16
 /* The L2 flush before every run: write `write_bytes` of one buffer (0 =
  * the default, 1.25 x L2), then optionally read `read_bytes` of another so
  * that the timed run starts with only CLEAN lines in L2 (default 0: no

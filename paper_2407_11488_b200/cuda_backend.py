@@ -157,7 +157,8 @@ class CudaTarget:
         self.prefetch_depth = prefetch_depth or 4 * self.compiler.pool._max_workers
         self.stats = {"executed": 0, "gpu_ms": 0.0, "verify_failed": 0}
         self._slots_inflight: list = []  # execute_many: enqueued, not yet collected
-        self.pipeline_depth = 4          # configurations enqueued at once (<= rt.SLOTS)
+        # configurations enqueued at once (<= rt.SLOTS); TSG_PIPELINE_DEPTH overrides
+        self.pipeline_depth = int(os.environ.get("TSG_PIPELINE_DEPTH", "4"))
 
     # -- answer ------------------------------------------------------------------
     def _load(self, image: bytes):

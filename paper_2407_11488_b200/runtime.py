@@ -107,7 +107,7 @@ SIGNATURES = {
     "tsg_set_flush_bytes": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
 }
 
-SLOTS = 8  # include/tsgpu.h TSG_SLOTS (pipelined submission slots)
+SLOTS = 16  # include/tsgpu.h TSG_SLOTS (pipelined submission slots)
 
 _lib = None
 _lib_lock = threading.Lock()
