@@ -334,7 +334,7 @@ def our_arm(args, dist: Dist):
     prob = make_problem(args.workload)
     t_setup = time.perf_counter()
     target = CudaTarget(prob, device=dev, compiler=compiler)
-    target.retire_cap = 1 << 14  # no batch unload inside any timed region (flushed at close)
+    target.retire_cap = int(os.environ.get("TSG_RETIRE_CAP", 1 << 14))  # default: no batch unload inside the timed region
     setup_s = time.perf_counter() - t_setup
     proto = MeasurementProtocol(warmup_runs=1, benchmark_runs=7, flush_l2=True)
     peaks = measured_peaks()
