@@ -377,6 +377,11 @@ def our_arm(args, dist: Dist):
         f.result()
     precompile_s = time.perf_counter() - t0
 
+    # unload the warm-up steps' modules first (untimed cleanup): resident
+    # modules accumulate and slow module load/launch (measured on the e2e pass)
+    if os.environ.get("TSG_PRE_FLUSH_MODULES", "1") != "0":
+        target.flush_modules()
+
     # -- timed region -----------------------------------------------------------
     launches0 = dev.launch_count
     results = []
