@@ -49,6 +49,13 @@ def test_pipelined_matches_sequential(device):
                 # same kernel, same protocol: times agree to within noise
                 assert 0.5 < o.time_ms / seq[c].time_ms < 2.0, (c, o.time_ms, seq[c].time_ms)
         assert sum(o.ok for _, o in pip) >= 0.9 * len(configs)
+        # device timeline (tsg_slot_timeline): submissions run in order,
+        # back to back, each containing its 1 + 3 runs
+        tl = [tgt.extras[",".join(map(str, c))] for c, o in pip if o.ok]
+        for a, b in zip(tl, tl[1:]):
+            assert a["t_dev_start_ms"] < a["t_dev_end_ms"] <= b["t_dev_start_ms"] + 1e-3
+        for (c, o), x in zip([co for co in pip if co[1].ok], tl):
+            assert x["t_dev_end_ms"] - x["t_dev_start_ms"] >= 0.99 * sum(o.times_ms)
         # and the outputs really are the verified ones
         st, out = tgt.run_output(configs[0])
         assert st is Status.OK and np.array_equal(out, want)
