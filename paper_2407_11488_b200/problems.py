@@ -641,8 +641,10 @@ class Dedispersion(Problem):
         self.max_shift = int(dm_shifts(self.delay, dms, self.dm_first, self.dm_step).max())
         self.in_w = samples + self.max_shift
         # slack: grid-overshoot reads of the generic kernel (128) and the
-        # window kernel's staged row segments (<= 32*4 + block DM spread + 8)
-        self.pitch = ((samples + self.max_shift + 640 + 31) // 32) * 32
+        # staged row segments of the window / staged generic kernels: a block
+        # row starts at (first sample + its first DM's shift) & ~3 and spans
+        # <= 128 samples + the block's DM spread (<= max_shift) + 8
+        self.pitch = ((samples + self.max_shift + max(640, self.max_shift + 160) + 31) // 32) * 32
         self.seed = seed
 
     def data(self) -> np.ndarray:

@@ -51,3 +51,52 @@ def test_asm_dispatch_source_compiles_for_sm100a():
     assert "#define DD_HAVE_ASM" not in p.source_for(dict(zip(names, (32, 32, 2, 4, 1, 0))))
     odd = dict(zip(names, (32, 32, 3, 8, 1, 0)))
     assert "#define DD_HAVE_ASM" not in p.source_for(odd)  # odd TSX keeps the C++ switch
+
+
+def test_staged_generic_selection_and_smem():
+    """Host side of the staged generic kernel (kernels/dedispersion.cu DD_STG):
+    window and staged modes are exclusive, the selection rule is the measured
+    one, the ring depth is the deepest (<= 5) that fits 200 KiB, and the
+    smem size matches the kernel's layout (stages of CC rows of ROWLEN floats,
+    2 x NSTAGE mbarriers, the delay table)."""
+    import collections
+
+    p = Dedispersion()
+    names = p.space.param_names
+    seen = collections.Counter()
+    for c in p.space.enumerate_configs():
+        cfg = dict(zip(names, c))
+        d = p.config_defines(cfg)
+        assert not ("DD_WIN" in d and "DD_STG" in d)
+        ns = p.staged_stages(cfg)
+        if "DD_WIN" in d:
+            seen["window"] += 1
+            continue
+        rule = cfg["block_size_x"] >= 4 and cfg["block_size_x"] * cfg["tile_size_x"] >= 12 \
+            and cfg["tile_size_x"] * cfg["tile_size_y"] >= 8
+        assert bool(ns) == rule, c
+        if not ns:
+            assert p.smem_bytes(cfg) == 0
+            seen["plain"] += 1
+            continue
+        seen["staged"] += 1
+        assert d["DD_STG"] == 1 and d["DD_NSTAGE"] == ns and 2 <= ns <= 5
+        rowlen = (cfg["block_size_x"] * cfg["tile_size_x"] + p.block_span(cfg) + 4 + 3) & ~3
+        want = 4 * ns * 32 * rowlen + 16 * ns + 4 * p.NCH
+        assert p.smem_bytes(cfg) == want <= 200 * 1024
+        if ns < 5:  # one stage deeper would not fit
+            assert 4 * (ns + 1) * 32 * rowlen + 16 * (ns + 1) + 4 * p.NCH > 200 * 1024
+        # staged rows stay inside the padded input row (no read past the pitch)
+        assert p.NSAMP - 1 + p.max_shift + rowlen + 3 <= p.pitch
+    assert seen["staged"] > 2000 and seen["plain"] > 5000 and seen["window"] > 0
+
+
+def test_staged_mode_env_overrides(monkeypatch):
+    p = Dedispersion()
+    cfg = dict(zip(p.space.param_names, (2, 48, 3, 4, 1, 1)))  # narrow: plain by the rule
+    assert p.staged_stages(cfg) == 0
+    monkeypatch.setenv(Dedispersion.STAGED_ENV, "all")
+    assert p.staged_stages(cfg) > 0 and "DD_STG" in p.config_defines(cfg)
+    monkeypatch.setenv(Dedispersion.STAGED_ENV, "0")
+    wide = dict(zip(p.space.param_names, (16, 64, 4, 3, 1, 0)))
+    assert p.staged_stages(wide) == 0 and "DD_STG" not in p.config_defines(wide)
