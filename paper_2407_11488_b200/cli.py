@@ -138,10 +138,14 @@ def tune(space_path, backend_spec, strategy, budget, seed, out_path, device, sch
         if strategy == "brute" and (world > 1 or resume_path):
             from .multigpu import sharded_sweep, merged_result, torch_dist_plumbing
 
+            import glob
+
             st, gather, rank, world = torch_dist_plumbing()
+            mine = f"{resume_path}.rank{rank}" if resume_path and world > 1 else resume_path
+            # every log of an earlier run counts (one file, or one per rank)
+            earlier = sorted(set(glob.glob(f"{resume_path}.rank*")) | {resume_path}) if resume_path else []
             trace, _ = sharded_sweep(space, list(space.enumerate_configs()), backend, protocol, chunk, st,
-                                     gather, f"{resume_path}.rank{rank}" if resume_path and world > 1
-                                     else resume_path, rank)
+                                     gather, mine, rank, resume_from=earlier)
             result = merged_result(trace)
             cache = strategies.result_to_cache(space, result, strategies.default_device_name(backend, device),
                                                metadata)

@@ -67,17 +67,26 @@ class ChunkQueue:
 
 def sharded_sweep(space, configs: list, backend: BackendDescriptor, protocol: MeasurementProtocol,
                   chunk: int = 8, store=None, gather=None, log_path: str | None = None,
-                  rank: int = 0) -> tuple:
+                  rank: int = 0, resume_from=()) -> tuple:
     """Measure ``configs`` (in order) across ranks; returns (merged trace, stats).
 
     ``store``: a torch.distributed Store shared by the ranks (None = one
     process); ``gather(obj) -> list`` all-gathers a picklable object
     (None = one process).  Each rank returns the full merged trace.
+    ``log_path``: this rank's observation log (appended to, and resumed
+    from); ``resume_from``: further logs (e.g. the other ranks' of an
+    earlier run) whose observations also count as done -- the dynamic
+    queue hands chunks to different ranks on a restart.
     """
     import time
 
     log = ResultLog(log_path) if log_path else None
-    done = log.load() if log else {}
+    done = {}
+    for extra in resume_from:
+        if extra and extra != log_path:
+            done.update(ResultLog(extra).load())
+    if log:
+        done.update(log.load())
     q = ChunkQueue(len(configs), chunk, store)
     mine: list = []
     n_chunks = 0

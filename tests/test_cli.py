@@ -121,3 +121,36 @@ def test_tune_cuda_backend(tmp_path):
     r = CliRunner().invoke(cli, ["tune", "--space", "dedispersion", "--backend", "cuda:convolution",
                                  "--out", str(tmp_path / "bad.json")])
     assert r.exit_code != 0 and "does not match" in str(r.exception)
+
+
+def test_resume_counts_every_rank_log(golden, tmp_path):
+    """A restarted sweep treats observations in ANY earlier log (one per rank
+    of a multi-GPU run) as done: nothing is measured twice."""
+    from paper_2407_11488_b200.multigpu import sharded_sweep
+    from paper_2407_11488_b200.measure import MeasurementProtocol
+    from paper_2407_11488_b200.store import ResultLog
+
+    rec, s, spec, src = _setup(golden, tmp_path)
+    be = golden_backend(rec)[1]
+    configs = list(s.enumerate_configs())
+    # an earlier 2-rank run logged disjoint halves under <log>.rank0/.rank1
+    base = tmp_path / "obs.jsonl"
+    for r, part in enumerate((configs[::2], configs[1::2])):
+        lg = ResultLog(f"{base}.rank{r}")
+        for c in part:
+            lg.append(",".join(map(str, c)), be.cache.records[",".join(map(str, c))])
+        lg.close()
+    calls = []
+    be2 = golden_backend(rec)[1]
+    orig = be2.cache.records.get
+
+    class Spy(dict):
+        def get(self, k, d=None):
+            calls.append(k)
+            return orig(k, d)
+
+    be2.cache.records = Spy(be2.cache.records)
+    trace, _ = sharded_sweep(s, configs, be2, MeasurementProtocol(), 3, log_path=f"{base}.rank0",
+                             resume_from=[str(base), f"{base}.rank0", f"{base}.rank1"])
+    assert [c for c, _ in trace] == configs
+    assert calls == []  # everything came from the logs
