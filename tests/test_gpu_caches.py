@@ -50,3 +50,29 @@ def test_gpu_convolution_cache_imports_into_reference(tmp_path, reference_pkg):
     assert ref.space_fingerprint == bundled_space("convolution").fingerprint()
     ffg = build_ffg(ref, rs)  # raises IncompleteCache unless every valid configuration is present
     assert ffg is not None
+
+
+def test_gpu_dedispersion_cache_is_complete(tmp_path):
+    """The whole dedispersion space (11,130 configurations) swept on a B200
+    through the tune command line (all verified bit-exact on the device)."""
+    space = bundled_space("dedispersion")
+    keys = {config_key(c) for c in space.enumerate_configs()}
+    native = loads_cache(_unzip("dedispersion.tunescape.json", tmp_path).read_text())
+    assert set(native.records) == keys and len(keys) == 11130
+    assert all(o.ok and o.time_ms > 0 and len(o.times_ms) == 7 for o in native.records.values())
+    kt = import_external_cache(_unzip("dedispersion.kerneltuner.json", tmp_path), expected_space=space)
+    assert set(kt.records) == keys
+    summary = json.loads((CACHES / "dedispersion.summary.json").read_text())
+    best = min(native.records.items(), key=lambda kv: kv[1].time_ms)
+    assert best[0] == ",".join(map(str, summary["best"]))
+
+
+def test_gpu_dedispersion_cache_imports_into_reference(tmp_path, reference_pkg):
+    from tunescape.landscape import build_ffg
+    from tunescape.paramspace import bundled_space as ref_space
+    from tunescape.store import import_external_cache as ref_import
+
+    rs = ref_space("dedispersion")
+    ref = ref_import(_unzip("dedispersion.kerneltuner.json", tmp_path), expected_space=rs)
+    assert len(ref.records) == 11130
+    assert build_ffg(ref, rs) is not None  # complete landscape
