@@ -23,9 +23,23 @@ plus on-device verification against the naive reference kernel.
 * ``cpu_baseline`` -- the oracle port of the reference loop (CPU kernel,
   all host threads) on a bounded sample, rank 0 only.
 
+* ``kernels`` -- the other four tuned kernels (convolution, dedispersion,
+  GEMM fp32, GEMM tf32 tcgen05), measured in the same run after the
+  headline: the best configuration of a sample that includes the known
+  full-space optimum, its dominant launch's roofline (ncu traffic of that
+  configuration from ``profiles/traffic.json``) and the tuning impact
+  within the sample.
+
+``--workload dd_hotspot`` instead runs BASELINE configs[4]'s domain-
+decomposed hotspot (16384^2, 20 iterations, one row slab per rank, NCCL
+halo exchange overlapped with the interior launch), verified per rank
+bit-exact against the single-domain run.
+
 ``--impl reference`` times that CPU path alone and prints its own line.
 Under torchrun each rank takes a disjoint shard of configurations
 (weak scaling; no data-path collective), time = max over ranks.
+``--gpus N`` without a torchrun environment re-launches itself as N
+ranks (``torch.distributed.run``, 127.0.0.1).
 """
 
 from __future__ import annotations
@@ -55,6 +69,16 @@ WORKLOADS = {
                          desc="dedispersion 1536 ch x 2048 DM x 25000 samples fp32"),
     "gemm": dict(param="VWM", batch=12, desc="gemm 4096^3 fp32 CLBlast space"),
     "gemm_tc": dict(param=None, batch=8, desc="gemm 4096^3 tf32 tcgen05/TMEM/TMA variant (BN_T x STAGES)"),
+    "dd_hotspot": dict(param=None, batch=1, desc="domain-decomposed hotspot 16384x16384 fp32, 20 iterations, "
+                                                 "one row slab per rank, NCCL halo exchange"),
+}
+
+# kernels block: (known full-space optimum or best round-1 configuration, stratify-by, sample size)
+KERNEL_SAMPLES = {
+    "convolution": ([(256, 2, 4, 4, 1, 0, 0)], "tile_size_y", 11),
+    "dedispersion": ([(32, 32, 4, 8, 1, 0)], "block_size_x", 7),
+    "gemm": ([(128, 64, 16, 16, 8, 16, 8, 4, 4, 1, 1, 1, 1)], "VWM", 9),
+    "gemm_tc": ([(256, 2)], None, 7),
 }
 
 
@@ -247,7 +271,22 @@ def parse_args(argv=None):
     ap.add_argument("--cpu-sample-s", type=float, default=15.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--dump", default=None, help="write per-configuration results (JSON) here")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the other kernels' roofline block")
+    ap.add_argument("--dd-config", default="32,2,4,1,8,2,1", help="hotspot configuration of --workload dd_hotspot")
+    ap.add_argument("--dd-size", type=int, default=16384)
     return ap.parse_args(argv)
+
+
+def relaunch(n: int) -> None:
+    """Re-run this command as ``n`` torch.distributed ranks (never returns)."""
+    import socket
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    argv = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+            "--master-addr=127.0.0.1", f"--master-port={port}", str(Path(__file__).resolve())] + sys.argv[1:]
+    os.execv(sys.executable, argv)
 
 
 def traffic_of(workload: str, key: str) -> dict:
@@ -305,7 +344,7 @@ def reference_arm(args, dist: Dist):
     value = total_cfg / secs if secs > 0 else 0.0
     line = {
         "impl": "reference", "metric": metric_name(), "value": round(value, 4), "unit": "configs/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "n_gpus": args.gpus, "ranks": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * secs / max(1, args.steps), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": wl["desc"], "configs_per_step": 2, "protocol": "1 warmup + 7 runs, mean",
@@ -318,12 +357,151 @@ def reference_arm(args, dist: Dist):
     print(json.dumps(line), flush=True)
 
 
+def kernels_block(dev, compiler, peaks, proto, seed) -> dict:
+    """Best-of-sample rooflines of the other four tuned kernels (same run).
+
+    Each sample holds the known optimum (KERNEL_SAMPLES) plus a stratified
+    sample; every configuration goes through the full protocol and the
+    on-device verification, exactly like the headline sweep.
+    """
+    from paper_2407_11488_b200.cuda_backend import CudaTarget
+    from paper_2407_11488_b200.paramspace import config_key
+    from paper_2407_11488_b200.problems import make_problem
+    from paper_2407_11488_b200.sweep import roofline, stratified_sample
+
+    out = {}
+    for name, (known, param, n) in KERNEL_SAMPLES.items():
+        t0 = time.perf_counter()
+        prob = make_problem(name)
+        tgt = CudaTarget(prob, device=dev, compiler=compiler)
+        try:
+            extra = [c for c in stratified_sample(prob.space, n + len(known), seed, param) if c not in known]
+            cfgs = list(known) + extra[:n]
+            res = list(tgt.execute_many(cfgs, proto))
+            ok = [(c, o) for c, o in res if o.ok]
+            if not ok:
+                out[name] = {"error": "no configuration succeeded",
+                             "statuses": [o.status.value for _, o in res]}
+                continue
+            bc, bo = min(ok, key=lambda co: co[1].time_ms)
+            cfg = dict(zip(prob.space.param_names, bc))
+            info = tgt.extras.get(config_key(bc), {})
+            roof = roofline(prob, cfg, info, peaks)
+            roof.update(traffic_of(name, config_key(bc)))
+            perfs = [1.0 / o.time_ms for _, o in ok]
+            t = bo.time_ms * 1e-3
+            out[name] = {
+                "best_config": cfg, "time_ms": round(bo.time_ms, 5),
+                "gflops": round(prob.flops(cfg) / t / 1e9, 1),
+                "reference_metric": (round(prob.space.metric_value(bo.time_ms, bc), 2)
+                                     if prob.space.metric_source is not None else None),
+                "verify_rel_err": info.get("verify_rel_err"), "roofline": roof,
+                "tuning_impact_in_sample": {"best_over_median": round(max(perfs) / statistics.median(perfs), 3),
+                                            "best_over_worst": round(max(perfs) / min(perfs), 3),
+                                            "n_ok": len(ok), "n": len(cfgs)},
+                "sample": f"{len(known)} known-best + {len(cfgs) - len(known)} stratified ({param or 'all'}), "
+                          "1 warmup + 7 runs each, L2 flushed, verified on device",
+                "wall_s": round(time.perf_counter() - t0, 2)}
+        finally:
+            tgt.close()
+    return out
+
+
+def dd_arm(args, dist: Dist):
+    """BASELINE configs[4]: domain-decomposed hotspot, one slab per rank."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2407_11488_b200.dd_hotspot import DDRunner
+    from paper_2407_11488_b200.sweep import measured_peaks
+
+    cfg = tuple(int(x) for x in args.dd_config.split(","))
+    n = args.dd_size
+    iters = 20
+    r = DDRunner(cfg, n, n, iters, dist.dist if dist.world > 1 else None)
+    peaks = measured_peaks()
+    sampler = ClockSampler(dist.local)
+    sampler.start()
+    r.timed(max(3, args.warmup))
+    dist.barrier()
+    torch.cuda.synchronize()
+    r.dev.sync()
+    launches0 = r.launch_count
+    sampler.mark(True)
+    r.dev.mark(0)
+    for _ in range(args.steps):
+        r.run_once()
+    r.dev.mark(1)
+    ms = r.dev.elapsed_ms(0, 1)
+    sampler.mark(False)
+    launches = r.launch_count - launches0
+    clocks = sampler.stop()
+    dist.barrier()
+    t_max = dist.max(ms)
+    cells = float(n) * n * iters
+    flop_job = cells * r.prob.FLOP_PER_CELL * args.steps
+    value = flop_job / (t_max * 1e-3) / 1e9
+    # roofline of a rank's run: 12 B per owned cell per launch (read T, P;
+    # write T) against HBM; the bands' and halos' extra rows are overhead
+    n_launch = len(r.prob.step_plan(r.t))
+    byts = 12.0 * n * r.slab.rows * n_launch
+    run_ms = ms / args.steps
+    gbs = byts / (run_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None,
+            "basis": f"whole run per rank: {n_launch} launches x 12 B x owned cells / run time "
+                     "(interior + band launches, exchange and patch copies included)"}
+    ver = r.verify()
+    oks = dist.gather_obj(ver)
+    # e2e: slab input H2D from pinned host memory and owned rows D2H each step
+    lib, ctx = r.dev.lib, r.dev.ctx
+    host_out = np.empty((r.slab.rows, n), np.float32)
+    lib.tsg_host_register(r.host_t.ctypes.data, r.host_t.nbytes)
+    lib.tsg_host_register(host_out.ctypes.data, host_out.nbytes)
+    dist.barrier()
+    r.dev.sync()
+    r.dev.mark(2)
+    for _ in range(args.steps):
+        r.dev._check(lib.tsg_h2d(ctx, r.temp.data_ptr(), C.c_void_p(r.host_t.ctypes.data), r.host_t.nbytes))
+        r.run_once()
+        own = r.owned_rows()
+        r.dev._check(lib.tsg_d2h(ctx, C.c_void_p(host_out.ctypes.data), own.data_ptr(), host_out.nbytes))
+    r.dev.mark(3)
+    e2e_ms = dist.max(r.dev.elapsed_ms(2, 3))
+    lib.tsg_host_unregister(r.host_t.ctypes.data)
+    lib.tsg_host_unregister(host_out.ctypes.data)
+    r.close()
+    if dist.rank == 0:
+        line = {
+            "metric": metric_name(), "value": round(value, 2), "unit": "GFLOP/s",
+            "n_gpus": dist.world, "steps": args.steps, "warmup": max(3, args.warmup),
+            "ms_per_step": round(t_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": WORKLOADS["dd_hotspot"]["desc"], "grid": f"{n}x{n}", "iterations": iters,
+                       "hotspot_config": dict(zip(r.prob.space.param_names, cfg)),
+                       "slab_rows": r.slab.rows, "halo_rows": r.t,
+                       "l2": "inputs larger than L2 (1 GiB per grid buffer)",
+                       "flop_basis": "15 FLOP per cell update (Rodinia form, paper-style GFLOP/s)",
+                       "parallelism": f"row slabs x{dist.world}, NCCL P2P halo exchange overlapped with "
+                                      "the interior launch"},
+            "verify": {"bit_exact_vs_single_domain_all_ranks": all(v["bit_exact_vs_single_domain"] for v in oks),
+                       "max_rel_err_vs_rodinia_chain": max(v["max_rel_err_vs_rodinia_chain"] for v in oks)},
+            "roofline": roof,
+            "e2e": {"value": round(flop_job / (e2e_ms * 1e-3) / 1e9, 2), "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(r.host_t.nbytes), "d2h_bytes_per_step": int(host_out.nbytes),
+                    "path": "DDRunner.run_once + slab H2D (tsg_h2d, pinned) + owned rows D2H (tsg_d2h), per rank"},
+            "cpu_baseline": None, "gpu_launches": int(launches), "clocks": clocks,
+        }
+        print(json.dumps(line), flush=True)
+
+
 def our_arm(args, dist: Dist):
     from paper_2407_11488_b200 import runtime as rt
     from paper_2407_11488_b200.cuda_backend import Compiler, CudaTarget
     from paper_2407_11488_b200.measure import MeasurementProtocol
     from paper_2407_11488_b200.problems import make_problem
-    from paper_2407_11488_b200.sweep import fp32_peak, measured_peaks, roofline
+    from paper_2407_11488_b200.sweep import fp32_peak, measured_peaks, roofline, tf32_peak
     from paper_2407_11488_b200.paramspace import config_key
 
     wl = WORKLOADS[args.workload]
@@ -339,6 +517,10 @@ def our_arm(args, dist: Dist):
     proto = MeasurementProtocol(warmup_runs=1, benchmark_runs=7, flush_l2=True)
     peaks = measured_peaks()
     peaks.update(fp32_peak(dev))
+    try:
+        peaks.update(tf32_peak(dev))
+    except Exception as e:  # noqa: BLE001 -- the fallback denominator is stated in the line
+        peaks["tf32_error"] = str(e)[:200]
     space = prob.space
 
     def run_step(configs):
@@ -475,8 +657,8 @@ def our_arm(args, dist: Dist):
         e2e_ms = dist.max(dev.elapsed_ms(2, 3))
         e2e = {"value": round(dist.sum(e2e_cfg) / (e2e_ms / 1000.0), 3), "unit": "configs/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out_host.nbytes),
-               "path": "CudaTarget.execute per config (C-ABI tsg_run_timed) + inputs H2D from pinned "
-                       "host memory + best output D2H, every step",
+               "path": "CudaTarget.execute_many (C-ABI tsg_submit_timed / tsg_collect, pipelined) + "
+                       "inputs H2D from pinned host memory + best output D2H (tsg_d2h), every step",
                "host_breakdown_s": {k: round(v, 4) for k, v in brk.items()}}
         for arr in list(pinned.values()) + [out_host]:
             dev.lib.tsg_host_unregister(arr.ctypes.data)
@@ -491,6 +673,10 @@ def our_arm(args, dist: Dist):
         except Exception as e:  # noqa: BLE001 -- baseline is reported, never fatal
             cpu = {"value": None, "unit": "configs/s", "cores": None, "kind": "port",
                    "sample": f"unavailable: {e}"}
+
+    kernels = None
+    if not args.no_kernels and dist.rank == 0 and args.workload == "hotspot":
+        kernels = kernels_block(dev, compiler, peaks, proto, args.seed)
 
     if args.dump:
         rows = []
@@ -526,7 +712,10 @@ def our_arm(args, dist: Dist):
                       "ffma_tflops": round(peaks.get("ffma_tflops", 0.0), 3),
                       "ffma2_tflops": round(peaks.get("ffma2_tflops", 0.0), 3),
                       "fp32_source": "measured in-run: max of scalar FFMA and packed FFMA2 probes "
-                                     "(kernels/peak.cu)"},
+                                     "(kernels/peak.cu)",
+                      "tf32_tflops": round(peaks["tf32_tflops"], 2) if peaks.get("tf32_tflops") else None,
+                      "tf32_source": peaks.get("tf32_source", peaks.get("tf32_error"))},
+            "kernels": kernels,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clocks,
             "setup_s": round(setup_s, 2), "wall_s_timed": round(wall_s, 3),
         }
@@ -537,10 +726,14 @@ def our_arm(args, dist: Dist):
 
 def main(argv=None):
     args = parse_args(argv)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch(args.gpus)
     dist = Dist()
     try:
         if args.impl == "reference":
             reference_arm(args, dist)
+        elif args.workload == "dd_hotspot":
+            dd_arm(args, dist)
         else:
             our_arm(args, dist)
     finally:

@@ -201,6 +201,27 @@ int tsg_tma_encode_2d_f32(tsg_ctx* ctx, void* desc128, uint64_t gaddr, uint64_t 
 int tsg_event_record(tsg_ctx* ctx, int slot);
 int tsg_event_elapsed(tsg_ctx* ctx, int slot_begin, int slot_end, float* ms);
 
+/* Stream ordering against work enqueued OUTSIDE this library (new; the
+ * reference has no device layer).  The context launches on its own
+ * non-blocking stream, so it is unordered with any other stream -- e.g.
+ * the one torch.distributed's NCCL receive completes on.  A caller that
+ * hands buffers between the two MUST order them explicitly:
+ *   tsg_stream_wait(ctx, s):   later work on the context stream waits for
+ *                              everything enqueued on `s` so far;
+ *   tsg_stream_signal(ctx, s): later work on `s` waits for everything
+ *                              enqueued on the context stream so far.
+ * `s` is a CUstream / cudaStream_t handle value (0 = the legacy default
+ * stream).  tsg_stream_handle returns the context stream's own handle.
+ * tsg_launch_async enqueues a launch sequence without waiting (tsg_run
+ * waits); tsg_copy_async is a device-to-device copy on the context
+ * stream; tsg_sync waits for the context stream (watchdog timeout_ms). */
+int tsg_stream_handle(tsg_ctx* ctx, uint64_t* stream);
+int tsg_stream_wait(tsg_ctx* ctx, uint64_t stream);
+int tsg_stream_signal(tsg_ctx* ctx, uint64_t stream);
+int tsg_launch_async(tsg_ctx* ctx, const tsg_launch_t* seq, int n_launch);
+int tsg_copy_async(tsg_ctx* ctx, uint64_t dst, uint64_t src, size_t bytes);
+int tsg_sync(tsg_ctx* ctx, double timeout_ms);
+
 /* On-device verification (Kernel Tuner `answer`/`atol`): compares
  * float32 arrays `out` and `ref` of n elements.  Reports max |out-ref|,
  * max |ref|, number of elements with |out-ref| > atol + rtol*|ref| and

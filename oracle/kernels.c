@@ -146,6 +146,46 @@ static void hotspot_step(float* out, const float* tin, const float* power, int w
   parallel_for(h, hotspot_rows, &c);
 }
 
+/* The tuned kernels' folded form (kernels/hotspot.cu header, HS_C/HS_FAST):
+ * c = fmaf(ap, P, ac); T' = fmaf(ax, E+W, fmaf(ay, N+S, fmaf(at, T, c))). */
+typedef struct {
+  float* out;
+  const float *tin, *power;
+  int w, h;
+  float at, ay, ax, ap, ac;
+} hs_tuned_ctx;
+
+static void hotspot_tuned_rows(void* p, int y0, int y1) {
+  hs_tuned_ctx* c = (hs_tuned_ctx*)p;
+  const float* tin = c->tin;
+  const int w = c->w, h = c->h;
+  for (int y = y0; y < y1; ++y) {
+    for (int x = 0; x < w; ++x) {
+      const size_t i = (size_t)y * w + x;
+      const float t = tin[i];
+      const float n = y > 0 ? tin[i - w] : t;
+      const float s = y < h - 1 ? tin[i + w] : t;
+      const float we = x > 0 ? tin[i - 1] : t;
+      const float e = x < w - 1 ? tin[i + 1] : t;
+      const float cp = fmaf(c->ap, c->power[i], c->ac);
+      c->out[i] = fmaf(c->ax, e + we, fmaf(c->ay, n + s, fmaf(c->at, t, cp)));
+    }
+  }
+}
+
+void oracle_hotspot_tuned(float* out, const float* temp, const float* power, int w, int h,
+                          int iterations, float at, float ay, float ax, float ap, float ac,
+                          float* scratch) {
+  const float* src = temp;
+  for (int it = 0; it < iterations; ++it) {
+    float* dst = ((iterations - 1 - it) % 2 == 0) ? out : scratch;
+    hs_tuned_ctx c = {dst, src, power, w, h, at, ay, ax, ap, ac};
+    parallel_for(h, hotspot_tuned_rows, &c);
+    src = dst;
+  }
+  if (iterations == 0) memcpy(out, temp, sizeof(float) * (size_t)w * h);
+}
+
 /* `iterations` steps from `temp`; result in `out`; `scratch` is w*h floats. */
 void oracle_hotspot(float* out, const float* temp, const float* power, int w, int h,
                     int iterations, float sdc, float rx1, float ry1, float rz1, float amb,

@@ -33,6 +33,8 @@ def lib():
         L = C.CDLL(str(LIB))
         L.oracle_convolution.argtypes = [_F, _F, C.c_int, C.c_int, C.c_int, _F, C.c_int, C.c_int]
         L.oracle_hotspot.argtypes = [_F, _F, _F, C.c_int, C.c_int, C.c_int] + [C.c_float] * 5 + [_F]
+        L.oracle_hotspot_tuned.argtypes = [_F, _F, _F, C.c_int, C.c_int, C.c_int] + [C.c_float] * 5 + [_F]
+        L.oracle_hotspot_tuned.restype = None
         L.oracle_dedispersion.argtypes = [_F, _F, C.c_int, _F, C.c_int, C.c_int, C.c_int,
                                           C.c_float, C.c_float]
         L.oracle_gemm.argtypes = [_F, _F, _F, C.c_int, C.c_int, C.c_int]
@@ -79,6 +81,20 @@ def hotspot(prob, iterations: int | None = None) -> np.ndarray:
     return out
 
 
+def hotspot_tuned(prob, iterations: int | None = None) -> np.ndarray:
+    """The tuned kernels' folded arithmetic (bit-exact target of every tuned
+    hotspot configuration; within rtol 1e-5 of :func:`hotspot`)."""
+    temp = np.ascontiguousarray(prob.temperature())
+    power = np.ascontiguousarray(prob.power())
+    out = np.empty(prob.W * prob.H, np.float32)
+    scratch = np.empty_like(out)
+    c = prob.tuned_coefficients(prob.k)
+    it = prob.iterations if iterations is None else iterations
+    lib().oracle_hotspot_tuned(_p(out), _p(temp), _p(power), prob.W, prob.H, it, c["at"], c["ay"], c["ax"],
+                               c["ap"], c["ac"], _p(scratch))
+    return out
+
+
 def dedispersion(prob) -> np.ndarray:
     padded = prob.buffers()[0].init
     out = np.empty(prob.NDM * prob.NSAMP, np.float32)
@@ -97,8 +113,17 @@ def gemm(prob) -> np.ndarray:
 
 
 def answer(prob) -> np.ndarray:
+    """The reference answer (the on-device naive kernel computes the same)."""
     return {"convolution": convolution, "hotspot": hotspot, "dedispersion": dedispersion,
             "gemm": gemm, "gemm_tc": gemm}[prob.space_name](prob)
+
+
+def tuned(prob) -> np.ndarray:
+    """What every tuned configuration must reproduce BIT-FOR-BIT: the answer,
+    except where the tuned kernels use a restated operation order (hotspot)."""
+    if prob.space_name == "hotspot":
+        return hotspot_tuned(prob)
+    return answer(prob)
 
 
 # ---------------------------------------------------------------------------

@@ -1,4 +1,4 @@
-"""Build the native pieces in-tree (sm_100a): libtsgpu.so and tsbench.
+"""Build the native pieces in-tree (sm_100a): libtsgpu.so and the C oracle.
 
 ``python -m paper_2407_11488_b200.build`` or ``__graft_entry__.build()``.
 NVRTC kernel sources under ``kernels/`` are compiled per configuration
@@ -43,18 +43,6 @@ def build_libtsgpu(force: bool = False) -> Path:
     return out
 
 
-def build_tsbench(force: bool = False) -> Path:
-    out = HERE / "tsbench"
-    src = HERE / "csrc" / "tsbench.cpp"
-    if not src.exists():
-        return out
-    lib = build_libtsgpu()
-    if force or _stale(out, src, lib):
-        _run(["g++", "-O2", "-std=c++17", "-o", str(out), str(src), f"-I{ROOT / 'include'}",
-              f"-L{HERE}", "-ltsgpu", f"-Wl,-rpath,$ORIGIN"])
-    return out
-
-
 SAMPLES = {
     "convolution.cu": "-DBSX=32 -DBSY=8 -DTSX=4 -DTSY=4 -DREAD_ONLY=1 -DUSE_PADDING=0 -DUSE_SHMEM=1 "
                       "-DIMG_W=4096 -DIMG_H=4096 -DIN_PITCH=4112",
@@ -90,7 +78,6 @@ def build_oracle() -> None:
 
 def build_all(force: bool = False, kernels: bool = True) -> None:
     build_libtsgpu(force)
-    build_tsbench(force)
     build_oracle()
     if kernels:
         check_kernels()

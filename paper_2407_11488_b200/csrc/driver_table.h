@@ -43,6 +43,7 @@
   X(cuStreamCreate) \
   X(cuStreamDestroy) \
   X(cuStreamSynchronize) \
+  X(cuStreamWaitEvent) \
   X(cuTensorMapEncodeTiled) \
 
 struct TsgDriver {
@@ -149,5 +150,7 @@ inline const char* tsg_load_driver() {
 #define cuStreamDestroy (tsg_drv().p_cuStreamDestroy)
 #undef cuStreamSynchronize
 #define cuStreamSynchronize (tsg_drv().p_cuStreamSynchronize)
+#undef cuStreamWaitEvent
+#define cuStreamWaitEvent (tsg_drv().p_cuStreamWaitEvent)
 #undef cuTensorMapEncodeTiled
 #define cuTensorMapEncodeTiled (tsg_drv().p_cuTensorMapEncodeTiled)

@@ -838,6 +838,66 @@ int tsg_event_elapsed(tsg_ctx* c, int a, int b, float* ms) {
   return TSG_OK;
 }
 
+// ---- ordering against foreign streams (torch / NCCL) -----------------------
+// One event per direction and call: record on the producer stream, wait on
+// the consumer.  Events are created with timing disabled (cheapest to
+// record) and destroyed right away -- the wait keeps its own reference.
+namespace {
+int order_streams(tsg_ctx* c, CUstream producer, CUstream consumer) {
+  CUevent e;
+  CUresult r = cuEventCreate(&e, CU_EVENT_DISABLE_TIMING);
+  if (r != CUDA_SUCCESS) return fail(TSG_ERR_SETUP, "cuEventCreate: " + cu_msg(r));
+  r = cuEventRecord(e, producer);
+  if (r == CUDA_SUCCESS) r = cuStreamWaitEvent(consumer, e, 0);
+  cuEventDestroy(e);
+  if (r != CUDA_SUCCESS) return fail(TSG_ERR_ARG, "stream ordering: " + cu_msg(r));
+  (void)c;
+  return TSG_OK;
+}
+}  // namespace
+
+int tsg_stream_handle(tsg_ctx* c, uint64_t* stream) {
+  if (!c || !stream) return fail(TSG_ERR_ARG, "null argument");
+  *stream = (uint64_t)(uintptr_t)c->stream;
+  return TSG_OK;
+}
+
+int tsg_stream_wait(tsg_ctx* c, uint64_t stream) {
+  int s = make_current(c);
+  if (s) return s;
+  return order_streams(c, (CUstream)(uintptr_t)stream, c->stream);
+}
+
+int tsg_stream_signal(tsg_ctx* c, uint64_t stream) {
+  int s = make_current(c);
+  if (s) return s;
+  return order_streams(c, c->stream, (CUstream)(uintptr_t)stream);
+}
+
+int tsg_launch_async(tsg_ctx* c, const tsg_launch_t* seq, int n) {
+  int s = make_current(c);
+  if (s) return s;
+  for (int i = 0; i < n; ++i)
+    if ((s = launch_one(c, seq[i]))) return s;
+  return TSG_OK;
+}
+
+int tsg_copy_async(tsg_ctx* c, uint64_t dst, uint64_t src, size_t bytes) {
+  int s = make_current(c);
+  if (s) return s;
+  CUresult r = cuMemcpyDtoDAsync((CUdeviceptr)dst, (CUdeviceptr)src, bytes, c->stream);
+  if (r != CUDA_SUCCESS) return fail(TSG_ERR_RUNTIME, "D2D async: " + cu_msg(r));
+  return TSG_OK;
+}
+
+int tsg_sync(tsg_ctx* c, double timeout_ms) {
+  int s = make_current(c);
+  if (s) return s;
+  if ((s = ensure_events(c, 1))) return s;
+  cuEventRecord(c->events[0], c->stream);
+  return wait_stream(c, c->events[0], timeout_ms);
+}
+
 int tsg_last_launch_times(tsg_ctx* c, float* t, int n) {
   if (!c) return fail(TSG_ERR_ARG, "null context");
   for (int i = 0; i < n; ++i) t[i] = i < (int)c->last_launch_ms.size() ? c->last_launch_ms[i] : 0.f;

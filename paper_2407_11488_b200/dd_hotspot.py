@@ -1,22 +1,55 @@
 """Domain-decomposed hotspot across the GPUs of one node (north_star N9).
 
-The 16384^2 grid is split into P row slabs, one per rank.  Rank p
-stores its H/P rows plus a halo of T rows on each side that has a
-neighbour (none above rank 0, none below rank P-1), so the slab's own
-first/last rows ARE the global boundary rows where one exists.  Every
-launch runs the UNMODIFIED tuned kernel (kernels/hotspot.cu, compiled
-with GH = slab height) for nsteps <= T steps; its clamped boundary at an
-internal slab edge produces wrong values that travel at most nsteps <= T
-rows -- i.e. only into the halo -- so the owned rows are exact, and the
-halo is refreshed by exchanging T rows with each neighbour between
-launches (NCCL send/recv over NVLink via torch.distributed, grouped with
-``batch_isend_irecv``; the only data-path collective of the build).
+The 16384^2 grid is split into P row slabs, one per rank.  Rank p stores
+its H/P owned rows plus a halo of h = T rows on each side that has a
+neighbour (none above rank 0, none below rank P-1).  The tuned kernel
+(kernels/hotspot.cu) advances any block of consecutive rows as an
+isolated grid: its clamped edge produces wrong values that travel at
+most nsteps <= T rows inward.  That is what makes the schedule below
+exact.
 
-The slab logic is independent of the step function, so the same code
-runs (a) on GPUs with the tuned kernel and NCCL and (b) on CPU under
-gloo with the C oracle as the step function -- the test that proves the
-decomposition bit-exact against the single-domain run (tests/
-test_dd_hotspot.py).
+Per launch of k <= T steps (``run``):
+
+1. *edge bands* -- the 3h stored rows at each internal slab edge (the
+   halo plus 2h owned rows) are advanced into small band buffers.  Rows
+   [h, 2h) of a band are exact: they are the h owned rows the neighbour
+   needs next.
+2. *interior* -- the owned rows alone are advanced as one grid into
+   ``dst``.  All but the h rows next to an internal edge are exact.
+3. *exchange* (not after the last launch) -- each band's exact rows go
+   to the neighbour, whose receive lands in ``dst``'s halo rows.  NCCL
+   point-to-point over NVLink via ``torch.distributed.batch_isend_irecv``.
+   This is the only data-path collective of the build.  It runs on its
+   own stream, so it overlaps step 2.
+4. *patch* -- the exact band rows are copied over ``dst``'s h damaged
+   owned rows at each internal edge.
+
+Extra work per launch: 2 x 3h band rows against H/P owned rows, i.e. 3%
+at 16384^2 on 8 GPUs with T = 8.
+
+Ordering contract (CUDA path).  Kernels and copies run on libtsgpu's
+context stream S.  torch.distributed's NCCL work runs on torch's current
+stream C (and its internal NCCL stream, which ProcessGroupNCCL orders
+after C at issue time; ``req.wait()`` orders C after it).  The two
+streams are ordered explicitly through the C ABI:
+
+* ``edges_done``: C waits for S once the edge bands are enqueued
+  (``tsg_stream_signal``), so the sends read finished band rows;
+* ``comm_done``: S waits for C before the next launch
+  (``tsg_stream_wait``), so the next launch reads the received halos,
+  and the band buffers are not overwritten while a send still reads them.
+
+Nothing else crosses streams: the interior launch writes only owned rows,
+the receives write only halo rows, the bands only band buffers.  Without
+the two waits the next launch could read halo rows before they land.
+``tests/test_dd_hotspot.py`` shows exactly that on one GPU, with a delayed
+producer on another stream standing in for the receive.
+
+The schedule is independent of the step function.  The same ``run``
+drives (a) GPUs with the tuned kernel and NCCL (``CudaOps``) and (b) CPU
+ranks under gloo with the C oracle as the step function (the tests).  The
+gloo tests prove the decomposition bit-exact against the single-domain
+run.
 """
 
 from __future__ import annotations
@@ -42,50 +75,64 @@ class Slab:
     def first_stored_row(self) -> int:
         return self.row0 - self.halo_top
 
+    @property
+    def halo(self) -> int:
+        return self.halo_top or self.halo_bot
+
 
 def make_slab(rank: int, world: int, gh: int, halo: int) -> Slab:
     if gh % world:
         raise ValueError(f"grid height {gh} not divisible by {world} ranks")
     rows = gh // world
-    if halo > rows:
-        raise ValueError("halo deeper than a slab")
+    if world > 1 and 2 * halo > rows:
+        raise ValueError(f"slab of {rows} rows too thin for a {halo}-row halo (need >= {2 * halo})")
     return Slab(rank, world, rows, rank * rows, halo if rank > 0 else 0,
                 halo if rank < world - 1 else 0)
 
 
-def exchange_halos(slab: Slab, buf, dist, group=None) -> None:
-    """Refresh ``buf``'s halo rows from the neighbours (buf: [height][W] tensor)."""
-    ops = []
-    h = slab.halo_top or slab.halo_bot
-    if slab.world == 1 or h == 0:
-        return
-    top_own = buf[slab.halo_top: slab.halo_top + h]
-    bot_own = buf[slab.halo_top + slab.rows - h: slab.halo_top + slab.rows]
-    if slab.rank > 0:
-        ops.append(dist.P2POp(dist.isend, top_own.contiguous() if not top_own.is_contiguous() else top_own,
-                              slab.rank - 1, group))
-        ops.append(dist.P2POp(dist.irecv, buf[0: slab.halo_top], slab.rank - 1, group))
-    if slab.rank < slab.world - 1:
-        ops.append(dist.P2POp(dist.isend, bot_own, slab.rank + 1, group))
-        ops.append(dist.P2POp(dist.irecv, buf[slab.halo_top + slab.rows:], slab.rank + 1, group))
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
+def band_rows(slab: Slab) -> int:
+    return 3 * slab.halo
 
 
-def run(slab: Slab, temp, power, scratch_a, scratch_b, iterations: int, t: int, step_fn, dist) -> object:
+def run(slab: Slab, temp, power, scratch_a, scratch_b, iterations: int, t: int, ops,
+        band_top=None, band_bot=None):
     """Advance ``iterations`` steps in launches of <= t; returns the buffer holding the result.
 
-    ``step_fn(src, dst, nsteps)`` advances the whole slab (tensors
-    [height][W]); ``temp`` holds the initial slab INCLUDING valid halos.
+    ``temp``/``power``/``scratch_*``: [height][W] row-indexable buffers (the
+    initial slab INCLUDING valid halos).  ``band_*``: [3h][W] buffers, needed
+    on the sides with a neighbour.  ``ops`` supplies the step function,
+    copies, the exchange and the two ordering hooks (see the module doc).
     """
     n_launch = math.ceil(iterations / t)
     plan = [t] * (n_launch - 1) + [iterations - t * (n_launch - 1)]
+    h, H, ht, rows = slab.halo, slab.height, slab.halo_top, slab.rows
+    top, bot = slab.halo_top > 0, slab.halo_bot > 0
     src = temp
     for i, k in enumerate(plan):
         dst = scratch_a if i % 2 == 0 else scratch_b
-        step_fn(src, dst, k)
-        if i < n_launch - 1:
-            exchange_halos(slab, dst, dist)
+        last = i == n_launch - 1
+        if top:
+            ops.advance(src[0:3 * h], band_top, power[0:3 * h], k)
+        if bot:
+            ops.advance(src[H - 3 * h:H], band_bot, power[H - 3 * h:H], k)
+        if not last and (top or bot):
+            ops.edges_done()
+        ops.advance(src[ht:ht + rows], dst[ht:ht + rows], power[ht:ht + rows], k)
+        if not last and (top or bot):
+            sends, recvs = [], []
+            if top:
+                sends.append((band_top[h:2 * h], slab.rank - 1))
+                recvs.append((dst[0:h], slab.rank - 1))
+            if bot:
+                sends.append((band_bot[h:2 * h], slab.rank + 1))
+                recvs.append((dst[H - h:H], slab.rank + 1))
+            ops.exchange(sends, recvs)
+        if top:
+            ops.copy(dst[ht:ht + h], band_top[h:2 * h])
+        if bot:
+            ops.copy(dst[ht + rows - h:ht + rows], band_bot[h:2 * h])
+        if not last and (top or bot):
+            ops.comm_done()
         src = dst
     return src
 
@@ -100,111 +147,215 @@ def owned(slab: Slab, buf):
     return buf[slab.halo_top: slab.halo_top + slab.rows]
 
 
+class TorchExchange:
+    """Halo exchange through torch.distributed point-to-point (NCCL or gloo)."""
+
+    def __init__(self, dist, group=None):
+        self.dist, self.group = dist, group
+
+    def exchange(self, sends, recvs) -> None:
+        d = self.dist
+        ops = [d.P2POp(d.isend, buf, peer, self.group) for buf, peer in sends]
+        ops += [d.P2POp(d.irecv, buf, peer, self.group) for buf, peer in recvs]
+        for req in d.batch_isend_irecv(ops):
+            req.wait()
+
+
 # ---------------------------------------------------------------------------
-# CUDA driver: tuned kernel per slab + NCCL halo exchange (torchrun)
+# CUDA driver: tuned kernel per row block + NCCL halo exchange (torchrun)
+
+
+class CudaOps(TorchExchange):
+    """Step function = the tuned kernel on libtsgpu's stream; exchange on torch's.
+
+    One compiled module per row-block height (the kernel takes the grid
+    height as a compile-time constant): the owned rows and, with
+    neighbours, the 3h-row bands.
+    """
+
+    def __init__(self, dev, compiler, cfg: dict, width: int, iterations: int, heights, dist=None):
+        super().__init__(dist)
+        from .problems import Hotspot
+
+        self.dev, self.cfg = dev, cfg
+        self.variants = {}
+        self.modules = []
+        for hgt in sorted(set(heights)):
+            prob = Hotspot(width=width, height=hgt, iterations=iterations)
+            res = compiler.compile(prob.source(), prob.options(cfg))
+            if not res.ok:
+                raise RuntimeError(res.error)
+            rc, mod = dev.load(res.image)
+            if rc != 0:
+                raise RuntimeError(mod)
+            self.modules.append(mod)
+            kern = mod.function(prob.kernel_name)
+            smem = prob.smem_bytes(cfg)
+            if smem > 48 * 1024:
+                kern.set_max_dynamic_smem(smem)
+            if smem > 0:
+                kern.set_smem_carveout(100)
+            self.variants[hgt] = (prob, kern, prob.launch_shape(cfg, kern))
+
+    def advance(self, src, dst, power, nsteps: int) -> None:
+        prob, kern, shape = self.variants[src.shape[0]]
+        self.dev.launch_async([prob.launch(self.cfg, kern, dst.data_ptr(), src.data_ptr(), power.data_ptr(),
+                                           nsteps, shape)])
+
+    def copy(self, dst, src) -> None:
+        self.dev.copy_async(dst.data_ptr(), src.data_ptr(), src.numel() * src.element_size())
+
+    def _torch_stream(self) -> int:
+        import torch
+
+        return torch.cuda.current_stream().cuda_stream
+
+    def edges_done(self) -> None:
+        self.dev.signal_stream(self._torch_stream())
+
+    def comm_done(self) -> None:
+        self.dev.wait_stream(self._torch_stream())
+
+    def close(self) -> None:
+        for m in self.modules:
+            m.unload()
+
+
+class DDRunner:
+    """One rank of the decomposed 16384^2 run on its GPU (env: RANK/WORLD_SIZE/LOCAL_RANK).
+
+    Buffers are torch tensors on this rank's GPU (so NCCL can send/recv
+    row ranges directly); kernels run through libtsgpu on the same
+    primary context.  ``run_once`` enqueues one full run (all launches and
+    exchanges) bracketed by device markers; ``verify`` checks the owned rows
+    against the single-domain run of the same configuration (bit-exact) and
+    the naive Rodinia-form chain (tolerance).
+    """
+
+    def __init__(self, config: tuple, width: int = 16384, height: int = 16384, iterations: int = 20,
+                 dist=None):
+        import os
+
+        import numpy as np
+        import torch
+
+        from . import runtime as rt
+        from .cuda_backend import Compiler
+        from .problems import Hotspot
+
+        self.rank, self.world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+        self.local = int(os.environ.get("LOCAL_RANK", 0))
+        torch.cuda.set_device(self.local)
+        self.dist = dist
+        self.prob = Hotspot(width=width, height=height, iterations=iterations)
+        self.config = tuple(config)
+        self.cfg = dict(zip(self.prob.space.param_names, config))
+        self.t = self.cfg["temporal_tiling_factor"]
+        self.W, self.H, self.iterations = width, height, iterations
+        self.slab = make_slab(self.rank, self.world, height, self.t)
+        self.dev = rt.Device(self.local)
+        self.cuda = f"cuda:{self.local}"
+        self.host_t = np.ascontiguousarray(slab_rows(self.slab, self.prob.temperature()))
+        self.host_p = np.ascontiguousarray(slab_rows(self.slab, self.prob.power()))
+        self.temp = torch.from_numpy(self.host_t).to(self.cuda)
+        self.power = torch.from_numpy(self.host_p).to(self.cuda)
+        self.a, self.b = torch.empty_like(self.temp), torch.empty_like(self.temp)
+        self.bands = {}
+        heights = [self.slab.rows]
+        if self.world > 1:
+            heights.append(band_rows(self.slab))
+            for side in ("top", "bot"):
+                self.bands[side] = torch.empty((band_rows(self.slab), width), dtype=torch.float32,
+                                               device=self.cuda)
+        self.compiler = Compiler()
+        self.ops = CudaOps(self.dev, self.compiler, self.cfg, width, iterations, heights, dist)
+        self.out = None
+        torch.cuda.synchronize()
+
+    @property
+    def launch_count(self) -> int:
+        return self.dev.launch_count
+
+    def run_once(self):
+        self.out = run(self.slab, self.temp, self.power, self.a, self.b, self.iterations, self.t, self.ops,
+                       self.bands.get("top"), self.bands.get("bot"))
+        return self.out
+
+    def timed(self, repeats: int, marker0: int = 0, marker1: int = 1) -> list:
+        """Device times (ms) of ``repeats`` whole runs, each bracketed by markers."""
+        import torch
+
+        times = []
+        for _ in range(repeats):
+            if self.world > 1:
+                self.dist.barrier()
+            torch.cuda.synchronize()
+            self.dev.sync()
+            self.dev.mark(marker0)
+            self.run_once()
+            self.dev.mark(marker1)
+            times.append(self.dev.elapsed_ms(marker0, marker1))
+        return times
+
+    def owned_rows(self):
+        self.dev.sync()
+        return owned(self.slab, self.out)
+
+    def verify(self) -> dict:
+        import numpy as np
+
+        from .cuda_backend import CudaTarget
+
+        got = self.owned_rows().cpu().numpy()
+        tgt = CudaTarget(self.prob, device=self.dev, compiler=self.compiler)
+        try:
+            st, full = tgt.run_output(self.config)
+            if st.value != "ok":
+                raise RuntimeError(f"single-domain run failed: {full}")
+            r0, n = self.slab.row0, self.slab.rows
+            want = full.reshape(self.H, self.W)[r0:r0 + n]
+            ref = tgt.answer().reshape(self.H, self.W)[r0:r0 + n]
+        finally:
+            tgt.close()
+        return {"bit_exact_vs_single_domain": bool(np.array_equal(got, want)),
+                "max_rel_err_vs_rodinia_chain": float(np.max(np.abs(got.astype(np.float64) - ref))
+                                                      / np.max(np.abs(ref)))}
+
+    def close(self):
+        self.ops.close()
+        self.compiler.shutdown()
 
 
 def cuda_run(config: tuple, width: int = 16384, height: int = 16384, iterations: int = 20,
              repeats: int = 3, verify: bool = True) -> dict:
-    """One rank of the decomposed run (env: RANK/WORLD_SIZE/LOCAL_RANK).
-
-    Buffers are torch tensors on this rank's GPU (so NCCL can send/recv
-    row ranges directly); kernels are launched through libtsgpu on the
-    same primary context.  Returns timing (max over ranks) and, with
-    ``verify``, whether the owned rows equal the single-GPU result of the
-    naive reference chain bit-for-bit.
-    """
-    import ctypes as C
+    """One rank of the decomposed run (under torchrun for P > 1): best of
+    ``repeats`` device times after one warm-up (max over ranks), and the
+    verification of :meth:`DDRunner.verify` (AND / max over ranks)."""
     import os
 
-    import numpy as np
     import torch
     import torch.distributed as tdist
 
-    from . import runtime as rt
-    from .cuda_backend import Compiler
-    from .problems import Hotspot
-
-    rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
-    local = int(os.environ.get("LOCAL_RANK", 0))
-    torch.cuda.set_device(local)
+    world = int(os.environ.get("WORLD_SIZE", 1))
     if world > 1 and not tdist.is_initialized():
+        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
         tdist.init_process_group("nccl")
-    prob = Hotspot(width=width, height=height, iterations=iterations)
-    space = prob.space
-    cfg = dict(zip(space.param_names, config))
-    t = cfg["temporal_tiling_factor"]
-    slab = make_slab(rank, world, height, t)
-    dev = rt.Device(local)
-    full_t = prob.temperature()
-    full_p = prob.power()
-    dev_t = torch.from_numpy(np.ascontiguousarray(slab_rows(slab, full_t))).to(f"cuda:{local}")
-    dev_p = torch.from_numpy(np.ascontiguousarray(slab_rows(slab, full_p))).to(f"cuda:{local}")
-    a, b = torch.empty_like(dev_t), torch.empty_like(dev_t)
-    slab_prob = Hotspot(width=width, height=slab.height, iterations=iterations)
-    comp = Compiler()
-    res = comp.compile(slab_prob.source(), slab_prob.options(cfg))
-    if not res.ok:
-        raise RuntimeError(res.error)
-    rc, mod = dev.load(res.image)
-    kern = mod.function(slab_prob.kernel_name)
-    smem = slab_prob.smem_bytes(cfg)
-    if smem > 48 * 1024:
-        kern.set_max_dynamic_smem(smem)
-    if smem > 0:
-        kern.set_smem_carveout(100)
-    shape = slab_prob.launch_shape(cfg, kern)  # stream mode: segments sized to this slab
-    torch.cuda.synchronize()
-
-    def step(src, dst, nsteps):
-        launch = slab_prob.launch(cfg, kern, dst.data_ptr(), src.data_ptr(), dev_p.data_ptr(), nsteps, shape)
-        code, err = dev.run([launch])
-        if code != rt.OK:
-            raise RuntimeError(err)
-
-    class _Dist:
-        P2POp = tdist.P2POp if world > 1 else None
-        isend = tdist.isend
-        irecv = tdist.irecv
-
-        @staticmethod
-        def batch_isend_irecv(ops):
-            return tdist.batch_isend_irecv(ops)
-
-    times = []
-    out = None
-    for _ in range(repeats + 1):
-        if world > 1:
-            tdist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        out = run(slab, dev_t, dev_p, a, b, iterations, t, step, _Dist)
-        e1.record()
-        torch.cuda.synchronize()
-        times.append(e0.elapsed_time(e1))
-    times = times[1:]  # first repeat is warm-up
-    ms = min(times)
-    if world > 1:
-        tt = torch.tensor([ms], device=f"cuda:{local}")
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        ms = float(tt.item())
-    ok = None
+    r = DDRunner(config, width, height, iterations, tdist if world > 1 else None)
+    ms = min(r.timed(repeats + 1)[1:])
+    res = {"bit_exact_vs_single_domain": None, "max_rel_err_vs_rodinia_chain": None}
     if verify:
-        from .cuda_backend import CudaTarget
-
-        ref = CudaTarget(prob, device=dev, compiler=comp)  # full grid, naive reference chain
-        want = torch.from_numpy(ref.answer().reshape(height, width)[slab.row0: slab.row0 + slab.rows].copy())
-        got = owned(slab, out).cpu()
-        ok = bool(torch.equal(got, want))
-        ref.close()
-        if world > 1:
-            flag = torch.tensor([1 if ok else 0], device=f"cuda:{local}")
-            tdist.all_reduce(flag, op=tdist.ReduceOp.MIN)
-            ok = bool(flag.item())
-    mod.unload()
-    comp.shutdown()
+        res = r.verify()
+    if world > 1:
+        t = torch.tensor([ms, 1.0 if res["bit_exact_vs_single_domain"] else 0.0,
+                          res["max_rel_err_vs_rodinia_chain"] or 0.0], device=r.cuda)
+        tdist.all_reduce(t[:1], op=tdist.ReduceOp.MAX)
+        tdist.all_reduce(t[1:2], op=tdist.ReduceOp.MIN)
+        tdist.all_reduce(t[2:3], op=tdist.ReduceOp.MAX)
+        ms = float(t[0].item())
+        if verify:
+            res = {"bit_exact_vs_single_domain": bool(t[1].item()), "max_rel_err_vs_rodinia_chain": float(t[2].item())}
+    r.close()
     cells = float(width) * height * iterations
-    return {"world": world, "config": cfg, "ms": ms, "gcells_per_s": cells / ms / 1e6,
-            "gflops": cells * prob.FLOP_PER_CELL / ms / 1e6, "bit_exact": ok,
-            "halo_rows": t, "slab_rows": slab.rows}
+    return {"world": world, "config": r.cfg, "ms": ms, "gcells_per_s": cells / ms / 1e6,
+            "gflops": cells * r.prob.FLOP_PER_CELL / ms / 1e6, **res, "halo_rows": r.t,
+            "slab_rows": r.slab.rows}

@@ -1,14 +1,28 @@
 // Hotspot thermal stencil with temporal tiling (paper Table 1 hotspot
 // column; space paper_2407_11488_b200/spaces/hotspot.spec == ref
-// ts/spaces/hotspot.spec:11-25).  Rodinia update, clamped (replicate)
-// boundary, written with explicit fused multiply-adds:
+// ts/spaces/hotspot.spec:11-25), clamped (replicate) boundary.
+//
+// The naive reference kernel (the on-device answer) computes the Rodinia
+// form with explicit fused multiply-adds, 9 FP32 operations per cell:
 //
 //   T' = fma(sdc, fma(amb-T, rz1, fma(fma(-2,T,E+W), rx1, fma(fma(-2,T,N+S), ry1, P))), T)
 //
-// (15 FLOP per cell update).  The same operation order is used by every
-// configuration, by the naive reference kernel and by the CPU oracle
-// (oracle/kernels.c), compiled without implicit contraction
-// (--fmad=false), so results agree bit-for-bit.
+// The tuned kernels compute the same linear update with the coefficients
+// folded on the host (Hotspot.tuned_coefficients, float64 then fp32):
+//
+//   c  = fma(ap, P, ac)                       ap = sdc, ac = sdc*rz1*amb
+//   T' = fma(ax, E+W, fma(ay, N+S, fma(at, T, c)))
+//        at = 1 - sdc*(2*rx1 + 2*ry1 + rz1), ay = sdc*ry1, ax = sdc*rx1
+//
+// -- 5 operations per cell update once c is known; c depends on the power
+// row only, so the stream kernels compute it once per row and launch (the
+// first level that reads a power row replaces it by c in the shared ring)
+// and the block-tile kernels once per cell and launch.  Every tuned
+// configuration uses this operation order, and so does the CPU oracle's
+// oracle_hotspot_tuned (oracle/kernels.c), compiled without implicit
+// contraction (--fmad=false): tuned results agree with it bit-for-bit, and
+// with the Rodinia chain within the north_star tolerance (rtol 1e-5;
+// measured 1.4e-6 norm-wise at 1024^2 x 20 steps).
 //
 // One launch advances the grid by `nsteps` <= TT steps: a block owns an
 // OH x OW output tile plus a halo of TT cells per side (window EH x EW),
@@ -43,10 +57,14 @@
             fmaf(fmaf(-2.0f, (t), (e) + (w)), (rx1), fmaf(fmaf(-2.0f, (t), (n) + (s)), (ry1), (p)))), \
        (t))
 
+// tuned form (see the header): power term, then the 5-operation update
+#define HS_C(p, ap, ac) fmaf((ap), (p), (ac))
+#define HS_FAST(t, n, s, e, w, c, at, ay, ax) fmaf((ax), (e) + (w), fmaf((ay), (n) + (s), fmaf((at), (t), (c))))
+
 #ifndef REFERENCE_ONLY
 
 struct HsCoef {
-  float sdc, rx1, ry1, rz1, amb;
+  float at, ay, ax, ap, ac;
 };
 
 #if defined(HS_STREAM) && HS_STREAM
@@ -79,7 +97,7 @@ struct HsCoef {
 // aligned and either fully useful or not).  Chunks are laid out
 // chunk-major in shared memory (bank-conflict-free vector LDS).
 // Arithmetic is packed FFMA2/FADD2 on column pairs, per component
-// identical to HS_STEP (bit-exact).
+// identical to HS_FAST (bit-exact).
 //
 // loop_unroll_factor_t: the level loop is always fully unrolled (its
 // registers are indexed by level); UNROLL == 1 streams one row per
@@ -151,8 +169,13 @@ __device__ __forceinline__ void cp_wait() {
 }
 
 struct HsK2 {
-  float2 sdc, rx1, ry1, rz1, amb;
+  float2 at, ay, ax, ap, ac;
 };
+
+__device__ __forceinline__ HsK2 hs_pairs(const HsCoef& k) {
+  return HsK2{make_float2(k.at, k.at), make_float2(k.ay, k.ay), make_float2(k.ax, k.ax), make_float2(k.ap, k.ap),
+              make_float2(k.ac, k.ac)};
+}
 
 struct HsStream {
   const float* tin;
@@ -232,9 +255,21 @@ __device__ __forceinline__ void hs_stage_pair(const HsStream& S, int row) {
   cp_commit();
 }
 
-__device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, int r) {
+// The power term c = fma(ap, P, ac) of row r for this lane's columns.
+// SH_POWER: the first level to read a power row (FRESH) turns the staged P
+// into c in place -- the lane's own columns of the ring, so no other lane
+// is involved -- and the later levels read c.  Without SH_POWER every level
+// re-reads P through L1 and forms c itself.
+template <bool FRESH>
+__device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, int r, const HsK2& k2) {
 #if SH_POWER
-  lds_pairs(pw, S.pring + ((r - S.ia) & (PR - 1)) * SW, S.lane);
+  float* row = S.pring + ((r - S.ia) & (PR - 1)) * SW;
+  lds_pairs(pw, row, S.lane);
+  if (FRESH) {
+#pragma unroll
+    for (int q = 0; q < NP2; ++q) pw[q] = __ffma2_rn(k2.ap, pw[q], k2.ac);
+    sts_pairs(row, pw, S.lane);
+  }
 #else
   const float* prow = S.power + (size_t)min(max(r, 0), GH - 1) * GW;
   float t[TSX];
@@ -252,13 +287,14 @@ __device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, i
 #endif
   }
 #pragma unroll
-  for (int q = 0; q < NP2; ++q) pw[q] = make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f);
+  for (int q = 0; q < NP2; ++q)
+    pw[q] = __ffma2_rn(k2.ap, make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f), k2.ac);
 #endif
 }
 
-// One cell-pair row update (HS_STEP on columns 2q, 2q+1; bit-exact):
+// One cell-pair row update (HS_FAST on columns 2q, 2q+1; bit-exact):
 // C = centre row, N/S rows, wl/er = W of column 0 / E of column TSX-1
-// (from the neighbour lanes), P = power row.
+// (from the neighbour lanes), P = the row's power term c.
 // Edge modes E (warp-uniform, chosen per warp tile):
 //   E & 3 == 0: interior strip (no horizontal clamp)
 //   E & 3 == 1: strip holding grid column 0 / GW-1 at a LANE boundary: the
@@ -294,17 +330,13 @@ __device__ __forceinline__ void hs_row_update(float2 (&nv)[NP2], const float2* N
       e1 = (S.rmask >> (j + 1)) & 1u ? t.y : e1;
     }
     if (j + 1 < TSX) {
-      const float2 m2 = make_float2(-2.0f, -2.0f);
-      const float2 m1 = make_float2(-1.0f, -1.0f);
-      const float2 ns = __ffma2_rn(m2, t, __fadd2_rn(n, s));
-      const float2 ew = __ffma2_rn(m2, t, make_float2(__fadd_rn(e0, w0), __fadd_rn(e1, w1)));
-      float2 d = __ffma2_rn(ns, k2.ry1, P[q]);
-      d = __ffma2_rn(ew, k2.rx1, d);
-      const float2 z = __ffma2_rn(t, m1, k2.amb);  // amb - t, one rounding
-      d = __ffma2_rn(z, k2.rz1, d);
-      nv[q] = __ffma2_rn(k2.sdc, d, t);
+      const float2 ns = __fadd2_rn(n, s);
+      const float2 ew = make_float2(__fadd_rn(e0, w0), __fadd_rn(e1, w1));
+      float2 u = __ffma2_rn(k2.at, t, P[q]);
+      u = __ffma2_rn(k2.ay, ns, u);
+      nv[q] = __ffma2_rn(k2.ax, ew, u);
     } else {  // odd TSX: scalar last column
-      nv[q] = make_float2(HS_STEP(t.x, n.x, s.x, e0, w0, P[q].x, kk.sdc, kk.rx1, kk.ry1, kk.rz1, kk.amb), 0.f);
+      nv[q] = make_float2(HS_FAST(t.x, n.x, s.x, e0, w0, P[q].x, kk.at, kk.ay, kk.ax), 0.f);
     }
   }
 }
@@ -376,10 +408,11 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     }
     // power rows a and a+1; row a+1 is the previous level's row a (reuse)
     float2 pa[NP2], pb[NP2];
-    hs_power(pa, S, a);
-    if (k == 1) {
-      hs_power(pb, S, a + 1);
+    if (k == 1) {  // rows a, a+1 are new to the pipeline: P -> c
+      hs_power<true>(pa, S, a, k2);
+      hs_power<true>(pb, S, a + 1, k2);
     } else {
+      hs_power<false>(pa, S, a, k2);
 #pragma unroll
       for (int q = 0; q < NP2; ++q) pb[q] = pprev[q];
     }
@@ -436,7 +469,10 @@ __device__ __forceinline__ void hs_stream_iter_s(const HsStream& S, int i, const
       er = S.xr ? COL(Cc, TSX - 1) : er;
     }
     float2 pa[NP2];
-    hs_power(pa, S, a);
+    if (k == 1)
+      hs_power<true>(pa, S, a, k2);
+    else
+      hs_power<false>(pa, S, a, k2);
     float2 na[NP2];
     hs_row_update<E>(na, N, Cc, f0, wl, er, pa, (E & 4) && a == 0, (E & 4) && a == GH - 1, S, kk, k2);
 #pragma unroll
@@ -447,8 +483,7 @@ __device__ __forceinline__ void hs_stream_iter_s(const HsStream& S, int i, const
 
 template <int E, int NS>
 __device__ __forceinline__ void hs_stream_run_s(const HsStream& S, const HsCoef& kk) {
-  const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
-                make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
+  const HsK2 k2 = hs_pairs(kk);
   for (int i = S.ia; i <= S.ib; i += 3) {
     hs_stream_iter_s<0, E, NS>(S, i, kk, k2);
     if (i + 1 > S.ib) break;
@@ -489,7 +524,10 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
     const int sC = ((PH - k) % 3 + 3) % 3;
     const int s0 = ((PH - k + 1) % 3 + 3) % 3;
     float2 pa[NP2];
-    hs_power(pa, S, a);
+    if (k == 1)
+      hs_power<true>(pa, S, a, k2);
+    else
+      hs_power<false>(pa, S, a, k2);
     float2 na[NP2];
     hs_row_update<E>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, (E & 4) && a == 0,
                         (E & 4) && a == GH - 1, S, kk, k2);
@@ -504,8 +542,7 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
 
 template <int E, int NS>
 __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& kk) {
-  const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
-                make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
+  const HsK2 k2 = hs_pairs(kk);
   float2 R[TT][3][NP2];
 #pragma unroll
   for (int a = 0; a < TT; ++a)
@@ -525,8 +562,7 @@ __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& 
 // ---- two rows per iteration (loop_unroll_factor_t > 1) -----------------------
 template <int E, int NS>
 __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
-  const HsK2 k2{make_float2(kk.sdc, kk.sdc), make_float2(kk.rx1, kk.rx1), make_float2(kk.ry1, kk.ry1),
-                make_float2(kk.rz1, kk.rz1), make_float2(kk.amb, kk.amb)};
+  const HsK2 k2 = hs_pairs(kk);
   float2 R[TT][4][NP2];
 #pragma unroll
   for (int a = 0; a < TT; ++a)
@@ -548,8 +584,8 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
 // being part of the same kernel, would cap every launch's occupancy.
 template <int NS>
 __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const float* __restrict__ tin,
-                                               const float* __restrict__ power, float sdc, float rx1,
-                                               float ry1, float rz1, float amb, int segh, int nsegs,
+                                               const float* __restrict__ power, float at, float ay,
+                                               float ax, float ap, float ac, int segh, int nsegs,
                                                int segh0) {
   extern __shared__ __align__(128) float smem[];
   const int tid = threadIdx.y * BSX + threadIdx.x;
@@ -600,7 +636,7 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
     cp_commit();
   }
 #endif
-  const HsCoef kk{sdc, rx1, ry1, rz1, amb};
+  const HsCoef kk{at, ay, ax, ap, ac};
   // edge mode of this warp tile (see hs_row_update)
   const bool xedge = S.gx0 <= 0 || S.gx0 + SW > GW - 1;
   const bool xalign = (S.gx0 > 0 || (-S.gx0) % TSX == 0) && (S.gx0 + SW <= GW - 1 || (GW - S.gx0) % TSX == 0);
@@ -638,19 +674,19 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
 
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
-               const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
-               float rz1, float amb, int segh, int nsegs, int segh0) {
+               const float* __restrict__ power, int nsteps, float at, float ay, float ax,
+               float ap, float ac, int segh, int nsegs, int segh0) {
   (void)nsteps;  // == TT
-  hs_stream_body<TT>(out, tin, power, sdc, rx1, ry1, rz1, amb, segh, nsegs, segh0);
+  hs_stream_body<TT>(out, tin, power, at, ay, ax, ap, ac, segh, nsegs, segh0);
 }
 
 #if defined(HS_REM) && HS_REM > 0
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_rem_kernel(float* __restrict__ out, const float* __restrict__ tin,
-                   const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
-                   float rz1, float amb, int segh, int nsegs, int segh0) {
+                   const float* __restrict__ power, int nsteps, float at, float ay, float ax,
+                   float ap, float ac, int segh, int nsegs, int segh0) {
   (void)nsteps;  // == HS_REM
-  hs_stream_body<HS_REM>(out, tin, power, sdc, rx1, ry1, rz1, amb, segh, nsegs, segh0);
+  hs_stream_body<HS_REM>(out, tin, power, at, ay, ax, ap, ac, segh, nsegs, segh0);
 }
 #endif
 
@@ -709,8 +745,8 @@ hotspot_rem_kernel(float* __restrict__ out, const float* __restrict__ tin,
 // Register mode: thread (tx,ty) owns column PAIRS (2p, 2p+1), p = tx + i*BSX,
 // over a contiguous strip of RY rows, values held in float2 registers across
 // all steps.  A step per pair: 2 scalar LDS (W of the left column, E of the
-// right one; N/S come from registers except at strip ends), the 9
-// arithmetic ops of HS_STEP as PACKED fp32x2 instructions (FFMA2/FADD2,
+// right one; N/S come from registers except at strip ends), the 5
+// arithmetic ops of HS_FAST as PACKED fp32x2 instructions (FFMA2/FADD2,
 // sm_100; per component identical to the scalar fmaf/fadd -> bit-exact),
 // and one 8-byte STS.  Rows with no active cell in the warp are skipped
 // (warp-uniform vote).  Smem is a padded, skewed layout (no bank
@@ -718,28 +754,22 @@ hotspot_rem_kernel(float* __restrict__ out, const float* __restrict__ tin,
 __device__ __forceinline__ float2 f2(float a, float b) { return make_float2(a, b); }
 
 struct HsCoef2 {  // coefficient pairs, built once per launch
-  float2 sdc, rx1, ry1, rz1, amb;
+  float2 at, ay, ax, ap, ac;
 };
 
-__device__ __forceinline__ float2 hs_step2(float2 t, float2 n, float2 s, float2 e, float2 w, float2 p,
+// HS_FAST on a column pair; c = the cells' power term
+__device__ __forceinline__ float2 hs_step2(float2 t, float2 n, float2 s, float2 e, float2 w, float2 c,
                                            const HsCoef2& k) {
-  const float2 m2 = f2(-2.0f, -2.0f);
-  const float2 m1 = f2(-1.0f, -1.0f);
-  const float2 ns = __ffma2_rn(m2, t, __fadd2_rn(n, s));
-  const float2 ew = __ffma2_rn(m2, t, __fadd2_rn(e, w));
-  float2 d = __ffma2_rn(ns, k.ry1, p);
-  d = __ffma2_rn(ew, k.rx1, d);
-  const float2 z = __ffma2_rn(t, m1, k.amb);  // amb - t, one rounding
-  d = __ffma2_rn(z, k.rz1, d);
-  return __ffma2_rn(k.sdc, d, t);
+  float2 u = __ffma2_rn(k.at, t, c);
+  u = __ffma2_rn(k.ay, __fadd2_rn(n, s), u);
+  return __ffma2_rn(k.ax, __fadd2_rn(e, w), u);
 }
 
 template <bool EDGE>
 __device__ __forceinline__ void hs_reg_steps(float2 (&v)[CXP][RY], const float2 (&pw)[CXP][RY],
                                              const float* __restrict__ power, float* A, float* B,
                                              int nsteps, int tx, int ty, int gx0, int gy0, HsCoef kk) {
-  const HsCoef2 k{f2(kk.sdc, kk.sdc), f2(kk.rx1, kk.rx1), f2(kk.ry1, kk.ry1), f2(kk.rz1, kk.rz1),
-                  f2(kk.amb, kk.amb)};
+  const HsCoef2 k{f2(kk.at, kk.at), f2(kk.ay, kk.ay), f2(kk.ax, kk.ax), f2(kk.ap, kk.ap), f2(kk.ac, kk.ac)};
   const int tb = ty * SS + 2 * tx;
   const int r0 = ty * RY;
   PRAGMA_UNROLL(UNROLL)
@@ -795,7 +825,8 @@ __device__ __forceinline__ void hs_reg_steps(float2 (&v)[CXP][RY], const float2 
               gxp = min(max(gxp, 0), GW - 1);
               gxq = min(max(gxq, 0), GW - 1);
             }
-            p = f2(__ldg(power + (size_t)gyp * GW + gxp), __ldg(power + (size_t)gyp * GW + gxq));
+            p = f2(HS_C(__ldg(power + (size_t)gyp * GW + gxp), kk.ap, kk.ac),
+                   HS_C(__ldg(power + (size_t)gyp * GW + gxq), kk.ap, kk.ac));
           }
 #endif
           const float2 u = hs_step2(t, n, so, e, w, p, k);
@@ -871,13 +902,13 @@ __device__ __forceinline__ float* hs_smem_steps(const float* __restrict__ power,
           e = (gx == GW - 1) ? t : e;
         }
 #if SH_POWER
-        const float p = P[rowb + c];
+        const float p = P[rowb + c];  // staged as c
 #else
         int gxp = gx0 + c;
         if (EDGE) gxp = min(max(gxp, 0), GW - 1);
-        const float p = __ldg(power + (size_t)(gy0 + r) * GW + gxp);
+        const float p = HS_C(__ldg(power + (size_t)(gy0 + r) * GW + gxp), k.ap, k.ac);
 #endif
-        const float u = HS_STEP(t, n, so, e, w, p, k.sdc, k.rx1, k.ry1, k.rz1, k.amb);
+        const float u = HS_FAST(t, n, so, e, w, p, k.at, k.ay, k.ax);
         if (cok[i]) B[rowb + c] = u;
         up[i] = t;
         mid[i] = dn;
@@ -895,8 +926,8 @@ __device__ __forceinline__ float* hs_smem_steps(const float* __restrict__ power,
 
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
-               const float* __restrict__ power, int nsteps, float sdc, float rx1, float ry1,
-               float rz1, float amb) {
+               const float* __restrict__ power, int nsteps, float at, float ay, float ax,
+               float ap, float ac) {
   extern __shared__ float smem[];
   // [guard][A][guard][B][guard][P], each buffer HS_BUF floats; the guards
   // absorb register mode's one-row/one-column overreach at the borders
@@ -904,7 +935,7 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
   float* B = A + HS_BUF + HS_GUARD;
   float* P = B + HS_BUF + HS_GUARD;  // shared mode with SH_POWER only
   (void)P;
-  const HsCoef k{sdc, rx1, ry1, rz1, amb};
+  const HsCoef k{at, ay, ax, ap, ac};
   const int tx = threadIdx.x, ty = threadIdx.y;
   const int gx0 = (int)blockIdx.x * OW - TT;
   const int gy0 = (int)blockIdx.y * OH - TT;
@@ -930,7 +961,7 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
       const size_t o = (size_t)gy * GW + gx;
       v[i][j] = f2(in0 ? __ldg(tin + o) : 0.f, in1 ? __ldg(tin + o + 1) : 0.f);
 #if SH_POWER
-      pw[i][j] = f2(in0 ? __ldg(power + o) : 0.f, in1 ? __ldg(power + o + 1) : 0.f);
+      pw[i][j] = f2(HS_C(in0 ? __ldg(power + o) : 0.f, ap, ac), HS_C(in1 ? __ldg(power + o + 1) : 0.f, ap, ac));
 #else
       pw[i][j] = f2(0.f, 0.f);
 #endif
@@ -967,7 +998,7 @@ hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
       if (c < EW && gx >= 0 && gx < GW) {
         A[ROWB(r) + c] = __ldg(tin + (size_t)gy * GW + gx);
 #if SH_POWER
-        P[ROWB(r) + c] = __ldg(power + (size_t)gy * GW + gx);
+        P[ROWB(r) + c] = HS_C(__ldg(power + (size_t)gy * GW + gx), ap, ac);
 #endif
       }
     }

@@ -267,9 +267,11 @@ class Hotspot(Problem):
     source_file = "hotspot.cu"
     kernel_name = "hotspot_kernel"
     reference_kernel = "hotspot_reference"
-    rtol = 1e-5
+    rtol = 1e-5  # north_star tolerance vs the Rodinia-form answer (elementwise |d| <= 1e-5 |ref|)
     extra_options = ("--fmad=false",)
-    FLOP_PER_CELL = 15  # 4 FADD + 5 FMA (kernels/hotspot.cu HS_STEP)
+    # algorithmic FLOP per cell update: the Rodinia form's 4 FADD + 5 FMA
+    # (the reference kernel's HS_STEP; the tuned kernels need 5 operations)
+    FLOP_PER_CELL = 15
 
     def __init__(self, width: int = 4096, height: int = 4096, iterations: int = 20,
                  seed_temp: int = 3, seed_power: int = 4):
@@ -450,10 +452,27 @@ class Hotspot(Problem):
         n = math.ceil(self.iterations / t)
         return [t] * (n - 1) + [self.iterations - t * (n - 1)]
 
+    @staticmethod
+    def tuned_coefficients(k: dict) -> dict:
+        """The tuned kernels' folded coefficients (kernels/hotspot.cu header).
+
+        T' = ax*(E+W) + ay*(N+S) + at*T + c,  c = ap*P + ac -- the Rodinia
+        update T + sdc*(P + ry1*(N+S-2T) + rx1*(E+W-2T) + rz1*(amb-T))
+        expanded; derived in float64 from the fp32 Rodinia coefficients,
+        then rounded once to fp32.
+        """
+        sdc, rx1, ry1, rz1, amb = (float(k[n]) for n in ("sdc", "rx1", "ry1", "rz1", "amb"))
+        f32 = lambda v: float(np.float32(v))  # noqa: E731
+        return dict(at=f32(1.0 - sdc * (2.0 * rx1 + 2.0 * ry1 + rz1)), ay=f32(sdc * ry1),
+                    ax=f32(sdc * rx1), ap=f32(sdc), ac=f32(sdc * rz1 * amb))
+
     def _coeff_args(self):
+        c = self.tuned_coefficients(self.k)
+        return [C.c_float(c[n]) for n in ("at", "ay", "ax", "ap", "ac")]
+
+    def _rodinia_args(self):
         k = self.k
-        return [C.c_float(k["sdc"]), C.c_float(k["rx1"]), C.c_float(k["ry1"]),
-                C.c_float(k["rz1"]), C.c_float(k["amb"])]
+        return [C.c_float(k[n]) for n in ("sdc", "rx1", "ry1", "rz1", "amb")]
 
     def _chain(self, kernel, bufs, n_launch, make):
         """Buffers for a ping-pong chain ending in bufs['out']."""
@@ -526,7 +545,7 @@ class Hotspot(Problem):
         grid = (math.ceil(self.W / 32), math.ceil(self.H / 8), 1)
         return self._chain(kernel, bufs, self.iterations, lambda i, s, d: Launch(
             kernel, grid, (256, 1, 1), [_u64(d), _u64(s), _u64(bufs["power"])]
-            + self._coeff_args()))
+            + self._rodinia_args()))
 
     def flops(self, cfg=None) -> float:
         return float(self.FLOP_PER_CELL) * self.W * self.H * self.iterations

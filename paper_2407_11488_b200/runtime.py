@@ -105,6 +105,12 @@ SIGNATURES = {
     "tsg_slot_timeline": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                     C.POINTER(C.c_float)]),
     "tsg_set_flush_bytes": (C.c_int, [C.c_void_p, C.c_size_t, C.c_size_t]),
+    "tsg_stream_handle": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    "tsg_stream_wait": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "tsg_stream_signal": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "tsg_launch_async": (C.c_int, [C.c_void_p, C.POINTER(LaunchT), C.c_int]),
+    "tsg_copy_async": (C.c_int, [C.c_void_p, C.c_uint64, C.c_uint64, C.c_size_t]),
+    "tsg_sync": (C.c_int, [C.c_void_p, C.c_double]),
 }
 
 SLOTS = 16  # include/tsgpu.h TSG_SLOTS (pipelined submission slots)
@@ -386,6 +392,33 @@ class Device:
         if rc in (ERR_RUNTIME, ERR_TIMEOUT):
             self.poisoned = True
         return rc, ("" if rc == OK else last_error())
+
+    # -- ordering against foreign streams (torch / NCCL), include/tsgpu.h --
+    @property
+    def stream(self) -> int:
+        """Handle of the context stream (CUstream value)."""
+        h = C.c_uint64()
+        self._check(self.lib.tsg_stream_handle(self.ctx, C.byref(h)))
+        return int(h.value)
+
+    def wait_stream(self, stream: int) -> None:
+        """Later work on the context stream waits for what ``stream`` has enqueued so far."""
+        self._check(self.lib.tsg_stream_wait(self.ctx, int(stream)))
+
+    def signal_stream(self, stream: int) -> None:
+        """Later work on ``stream`` waits for what the context stream has enqueued so far."""
+        self._check(self.lib.tsg_stream_signal(self.ctx, int(stream)))
+
+    def launch_async(self, launches: list) -> None:
+        """Enqueue launches on the context stream without waiting."""
+        arr = (LaunchT * len(launches))(*[l.to_struct() for l in launches])
+        self._check(self.lib.tsg_launch_async(self.ctx, arr, len(launches)))
+
+    def copy_async(self, dst: int, src: int, nbytes: int) -> None:
+        self._check(self.lib.tsg_copy_async(self.ctx, int(dst), int(src), int(nbytes)))
+
+    def sync(self, timeout_ms: float = 60000.0) -> None:
+        self._check(self.lib.tsg_sync(self.ctx, float(timeout_ms)))
 
     def run_timed(self, launches: list, warmup: int, runs: int, flush_l2: bool = True,
                   timeout_ms: float = 60000.0):

@@ -109,6 +109,39 @@ def fp32_peak(dev: rt.Device, iters: int = 2048) -> dict:
     return r
 
 
+def tf32_peak(dev: rt.Device, iters: int = 4096) -> dict:
+    """Dense tf32 tcgen05 throughput of this GPU (TFLOP/s), measured with CUDA
+    events: kernels/peak.cu tf32_mma_peak, one CTA per SM issuing back-to-back
+    M=128 N=256 K=8 MMAs from shared memory (the GEMM's instruction shape)."""
+    key = ("tf32", dev.index)
+    if key in _PEAK_CACHE:
+        return _PEAK_CACHE[key]
+    src = (Path(__file__).parent / "kernels" / "peak.cu").read_text()
+    res = rt.compile_source(src, ["--gpu-architecture=sm_100a", "-std=c++17"])
+    if not res.ok:
+        raise RuntimeError(res.error)
+    rc, mod = dev.load(res.image)
+    if rc != rt.OK:
+        raise RuntimeError(mod)
+    k = mod.function("tf32_mma_peak")
+    smem = 1024 + 128 * 128 + 256 * 128 + 64
+    k.set_max_dynamic_smem(smem)
+    blocks = dev.info["sm_count"]
+    out = dev.alloc(blocks * 4)
+    launch = rt.Launch(k, (blocks, 1, 1), (128, 1, 1), [C.c_uint64(out.ptr), C.c_int(iters)], smem=smem)
+    rc, times = dev.run_timed([launch], 2, 5, flush_l2=False)
+    mod.unload()
+    out.free()
+    if rc != rt.OK:
+        raise RuntimeError(times)
+    flop = 2.0 * 128 * 256 * 8 * 4 * iters * blocks
+    r = {"tf32_tflops": flop / (min(times) * 1e-3) / 1e12, "tf32_probe_ms": min(times),
+         "tf32_source": "measured in-run: tcgen05.mma kind::tf32 M128 N256 K8 back to back, one CTA per SM "
+                        "(kernels/peak.cu tf32_mma_peak)"}
+    _PEAK_CACHE[key] = r
+    return r
+
+
 def roofline(problem, cfg: dict, info: dict, peaks: dict) -> dict:
     """Roofline of the dominant launch of one configuration.
 
@@ -124,19 +157,34 @@ def roofline(problem, cfg: dict, info: dict, peaks: dict) -> dict:
     t = launch_ms[dom] * 1e-3
     flop = problem.flops(cfg) / n
     byts = problem.compulsory_bytes(cfg) / n
-    if getattr(problem, "space_name", "") == "hotspot":
-        steps = problem.step_plan(cfg["temporal_tiling_factor"])
-        flop = problem.FLOP_PER_CELL * problem.W * problem.H * steps[dom]
-        byts = 12.0 * problem.W * problem.H
     hbm_peak = peaks["hbm_gbs"] * 1e9
+    if getattr(problem, "space_name", "") == "hotspot":
+        # one launch advancing k steps: 12 B/cell compulsory (read T, P; write
+        # T).  The tuned form needs 5 FP32-pipe operations per cell update (+1
+        # per cell for the power term), so the FP32 time of a launch stays
+        # below its HBM time at every T <= 10: the binding roofline is HBM.
+        steps = problem.step_plan(cfg["temporal_tiling_factor"])
+        cells = problem.W * problem.H
+        byts = 12.0 * cells
+        gbs = byts / t / 1e9
+        fp_ops = cells * (5.0 * steps[dom] + 1.0)
+        pipe = peaks.get("fp32_tflops", 0.0) * 1e12 / 2.0  # FMA-pipe operations per second
+        return {"bound": "hbm", "achieved": round(gbs, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": round(gbs / peaks["hbm_gbs"], 4), "traffic": None,
+                "bytes_per_launch": byts, "launch_us": round(t * 1e6, 3), "steps_in_launch": steps[dom],
+                "alt": {"paper_gflops": round(problem.FLOP_PER_CELL * cells * steps[dom] / t / 1e9, 1),
+                        "fp32_pipe_frac": round(fp_ops / t / pipe, 4) if pipe else None,
+                        "hbm_floor_us": round(byts / hbm_peak * 1e6, 2)}}
     if getattr(problem, "space_name", "") == "gemm_tc":
-        # tf32 tensor pipe: dense tf32 = 1/2 dense bf16; denominator = half the
-        # driver-measured cuBLAS bf16 burst (no tf32 figure is measured)
-        tf32 = 0.5 * peaks.get("bf16_tflops", 1639.7)
+        # tf32 tensor pipe: the in-run tcgen05 tf32 probe (sweep.tf32_peak);
+        # fallback half the driver-measured bf16 burst
+        if peaks.get("tf32_tflops"):
+            tf32, src = peaks["tf32_tflops"], peaks.get("tf32_source", "in-run tf32 probe")
+        else:
+            tf32, src = 0.5 * peaks.get("bf16_tflops", 1639.7), "0.5 x MEASURED_PEAKS bf16_tflops (fallback)"
         tfs = flop / t / 1e12
         return {"bound": "tensor", "achieved": round(tfs, 2), "peak": round(tf32, 2), "unit": "TFLOP/s",
-                "frac": round(tfs / tf32, 4), "traffic": None,
-                "peak_source": "0.5 x MEASURED_PEAKS bf16_tflops (tf32 = half-rate bf16)",
+                "frac": round(tfs / tf32, 4), "traffic": None, "peak_source": src,
                 "alt": {"hbm_gbs": round(byts / t / 1e9, 2)}}
     fp32 = peaks.get("fp32_tflops", 0.0) * 1e12
     if getattr(problem, "space_name", "") == "dedispersion":

@@ -1,10 +1,14 @@
 """GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
 
 * small problems, many configurations per space (stratified, including
-  the extreme block shapes): kernel output BIT-EXACT vs the C oracle;
+  the extreme block shapes): kernel output BIT-EXACT vs the C oracle's
+  restatement of the tuned arithmetic (``K.tuned``: the answer itself,
+  except hotspot's folded-coefficient form, itself within 1e-6 of the
+  Rodinia answer -- tests/test_oracle.py);
 * full BASELINE sizes: the on-device answer kernel bit-exact vs the
-  oracle, then a sweep of configurations verified on-device (max
-  relative error stated in the test: 0 expected, 1e-5 tolerated);
+  oracle, then a sweep of configurations verified on-device against it
+  (tolerance stated in the test: rtol 1e-5 norm-wise; 0 expected except
+  for hotspot's folded form);
 * failure mapping: NVRTC error -> compile_failed, oversize launch ->
   invalid, never an exception.
 """
@@ -54,6 +58,7 @@ def test_small_problem_bit_exact(name, device):
     make, param, n = SMALL[name]
     prob = make()
     want = K.answer(prob)
+    tuned = K.tuned(prob)
     tgt = CudaTarget(prob, device=device, answer=want)
     try:
         ref = tgt.answer()
@@ -68,7 +73,7 @@ def test_small_problem_bit_exact(name, device):
                 continue
             st, out = tgt.run_output(c)
             assert st is Status.OK, (c, out)
-            diff = int(np.sum(out != want))
+            diff = int(np.sum(out != tuned))
             assert diff == 0, f"{name} {c}: {diff} elements differ"
             ok += 1
         assert ok >= 0.9 * len(configs)
@@ -92,8 +97,9 @@ def test_full_size_answer_and_sweep(name, device):
             assert obs.status in (Status.OK, Status.INVALID), (c, obs)
             if obs.ok:
                 rel = tgt.extras[",".join(map(str, c))]["verify_rel_err"]
-                assert rel <= 1e-5, (c, rel)  # tolerance: 1e-5 norm-wise; bit-exact expected
-                assert rel == 0.0, (c, rel)
+                assert rel <= 1e-5, (c, rel)  # tolerance: 1e-5 norm-wise
+                if name != "hotspot":  # hotspot: folded form, ~1e-6 (tests/test_oracle.py)
+                    assert rel == 0.0, (c, rel)
     finally:
         tgt.close()
 
@@ -118,8 +124,8 @@ def test_hotspot_stream_mode_bit_exact(device):
     every T (incl. the remainder launch of 20 % T), odd/even TSX, power in
     smem or through L1, grid edges -- bit-exact vs the C oracle."""
     prob = Hotspot(width=520, height=264, iterations=20)
-    want = K.answer(prob)
-    tgt = CudaTarget(prob, device=device, answer=want)
+    want = K.tuned(prob)
+    tgt = CudaTarget(prob, device=device, answer=K.answer(prob))
     try:
         configs = _stream_configs(prob)
         assert len(configs) >= 30
@@ -139,8 +145,8 @@ def test_hotspot_stream_smem_mode_bit_exact(device):
     register-heavy TT x TSX configurations): every T, odd/even TSX, both
     sh_power values -- bit-exact vs the C oracle."""
     prob = Hotspot(width=520, height=264, iterations=20)
-    want = K.answer(prob)
-    tgt = CudaTarget(prob, device=device, answer=want)
+    want = K.tuned(prob)
+    tgt = CudaTarget(prob, device=device, answer=K.answer(prob))
     try:
         configs = _stream_configs(prob, mode="stream_smem")
         assert len(configs) >= 12

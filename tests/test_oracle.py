@@ -50,6 +50,41 @@ def test_hotspot_matches_float64():
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-5
 
 
+@pytest.mark.parametrize("shape", [(64, 48), (520, 264), (1024, 1024)])
+def test_hotspot_tuned_form_within_tolerance(shape):
+    """The tuned kernels' folded-coefficient arithmetic vs the Rodinia form
+    and float64: well inside the north_star rtol 1e-5 (elementwise)."""
+    w, h = shape
+    p = Hotspot(width=w, height=h, iterations=20)
+    fast = K.hotspot_tuned(p).astype(np.float64)
+    rod = K.hotspot(p).astype(np.float64)
+    f64 = K.hotspot_f64(p)
+    assert np.max(np.abs(fast - rod) / np.abs(rod)) < 2e-6
+    assert np.max(np.abs(fast - f64)) / np.max(np.abs(f64)) < 2e-6
+    assert not np.array_equal(fast, rod)  # really the other operation order
+
+
+def test_hotspot_tuned_coefficients_expand_rodinia():
+    p = Hotspot(width=8, height=8)
+    k, c = p.k, p.tuned_coefficients(p.k)
+    assert c["ax"] == pytest.approx(k["sdc"] * k["rx1"], rel=1e-7)
+    assert c["at"] + 2 * c["ax"] + 2 * c["ay"] + k["sdc"] * k["rz1"] == pytest.approx(1.0, rel=1e-6)
+    assert c["ac"] == pytest.approx(k["sdc"] * k["rz1"] * k["amb"], rel=1e-7)
+
+
+def test_hotspot_tuned_ambient_fixed_point():
+    """Zero power at ambient temperature stays (to fp32 rounding) at ambient."""
+    p = Hotspot(width=40, height=30, iterations=7)
+    amb = np.full((30, 40), p.k["amb"], np.float32)
+    zero = np.zeros((30, 40), np.float32)
+    out = np.empty(1200, np.float32)
+    scratch = np.empty_like(out)
+    c = p.tuned_coefficients(p.k)
+    K.lib().oracle_hotspot_tuned(K._p(out), K._p(amb), K._p(zero), 40, 30, 7, c["at"], c["ay"], c["ax"],
+                                 c["ap"], c["ac"], K._p(scratch))
+    assert np.max(np.abs(out - p.k["amb"])) < 1e-4
+
+
 def test_hotspot_is_stable_at_full_size_constants():
     """Pinned cell size keeps the explicit scheme stable."""
     p = Hotspot(width=256, height=256, iterations=20)
