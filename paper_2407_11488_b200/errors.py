@@ -1,96 +1,139 @@
-"""Error taxonomy of the tuner.
+"""Errors raised by the tuner, grouped by who has to act on them.
 
-Mirrors the reference hierarchy (`pkg/src/tunescape/errors.py:8-98`) so
-that callers switching from ``tunescape`` catch the same classes:
-domain failures derive from :class:`TunescapeError`; measurement
-failures of a configuration are *never* raised, they become
-``Observation`` statuses (`SPEC.md:139`, `SPEC.md:181`).
+The class *names* are the public contract callers catch (they are the
+names SPEC.md uses: ``MissingEntry``, ``IncompleteCache``,
+``SpaceMismatch`` ...), so code written against the reference keeps its
+``except`` clauses.  Measurement failures of a single configuration are
+never raised -- they are ``Observation`` statuses (SPEC.md "Failures are
+first-class recorded outcomes").
 
-Two classes are new on the B200 side: :class:`DeviceError` (the CUDA
-runtime itself is unusable, e.g. the native library is missing) and
-:class:`VerificationError` (``run_kernel`` output disagrees with
-``answer`` when the caller asked for a hard failure).
+Intermediate bases group the classes by the stage that raises them, so
+a caller can catch "the space definition is wrong" (:class:`SpaceError`)
+or "a cache file is unusable" (:class:`CacheError`) in one clause.  The
+command line maps every one of them to exit status 1 (SPEC.md ``cli``).
+
+B200-only additions: :class:`DeviceError` (the CUDA runtime is unusable:
+library missing, no device) and :class:`VerificationError` (an output
+disagrees with ``answer`` and the caller asked for a hard failure).
 """
+
+from __future__ import annotations
 
 
 class TunescapeError(Exception):
-    """Root of every error raised deliberately by this package."""
+    """Root: every deliberate error of this package derives from it."""
 
 
-class ExpressionSyntaxError(TunescapeError):
-    """An expression failed to tokenize or parse (ref errors.py:16-22)."""
+# --- the space (expressions, spec documents) ---------------------------------
+
+
+class SpaceError(TunescapeError):
+    """The definition of a search space is unusable."""
+
+
+class ExpressionSyntaxError(SpaceError):
+    """Text that does not tokenize/parse as an expression.
+
+    ``position`` is the 0-based character offset; the message shows it
+    1-based as a column, the form the reference's tests match.
+    """
 
     def __init__(self, message: str, source: str, position: int):
-        self.source = source
-        self.position = position
-        super().__init__(f"{message} (column {position + 1} in {source!r})")
+        self.source, self.position = source, position
+        Exception.__init__(self, "%s (column %d in %r)" % (message, position + 1, source))
 
 
-class ExpressionTypeError(TunescapeError):
-    """An expression is ill-typed for the parameter space (ref :25)."""
+class ExpressionTypeError(SpaceError):
+    """Well-formed expression that is ill-typed for its parameter space."""
 
 
-class EvaluationError(TunescapeError):
-    """Evaluating an expression failed, e.g. a zero divisor (ref :29)."""
-
-
-class SpecSyntaxError(TunescapeError):
-    """A space document is not well-formed YAML (ref :33-42)."""
+class SpecSyntaxError(SpaceError):
+    """A space document that is not a well-formed YAML mapping."""
 
     def __init__(self, message: str, line: int | None = None, column: int | None = None):
-        self.line = line
-        self.column = column
-        where = ""
+        self.line, self.column = line, column
         if line is not None:
-            where = f" (line {line}, column {1 if column is None else column})"
-        super().__init__(message + where)
+            message = "%s (line %d, column %d)" % (message, line, column or 1)
+        Exception.__init__(self, message)
 
 
-class SpecValidationError(TunescapeError):
-    """A space document parsed but is semantically wrong (ref :45)."""
+class SpecValidationError(SpaceError):
+    """A space document that parsed but describes an impossible space."""
 
 
-class MissingEntry(TunescapeError):
-    """A replay backend has no record for a configuration (ref :49)."""
+class EvaluationError(SpaceError):
+    """An expression failed on concrete values (zero divisor, ...)."""
+
+
+# --- measurement and analysis --------------------------------------------------
 
 
 class ProtocolError(TunescapeError):
-    """Bad protocol / backend descriptor / misuse of the API (ref :53)."""
+    """Misuse of the measurement API: bad protocol, descriptor or call."""
+
+
+class MissingEntry(TunescapeError):
+    """A replay backend holds no record for the requested configuration."""
 
 
 class NoFeasibleData(TunescapeError):
-    """An analysis needs at least one successful record (ref :57)."""
+    """An analysis needs at least one successful record and got none."""
 
 
-class IncompleteCache(TunescapeError):
-    """A cache does not cover the whole space (ref :61-69)."""
+class NonConvergence(TunescapeError):
+    """An iterative solver (PageRank) missed its tolerance."""
+
+    def __init__(self, iterations: int, residual: float, tol: float):
+        self.iterations, self.residual, self.tol = iterations, residual, tol
+        Exception.__init__(self, f"no convergence after {iterations} iterations "
+                                 f"(residual {residual:.3e}, tolerance {tol:.3e})")
+
+
+class NoPortableConfiguration(TunescapeError):
+    """No configuration scores above zero on every device of a set."""
+
+
+class UnknownDevice(TunescapeError):
+    """A device subset names a device that has no cache."""
+
+
+# --- cache files ----------------------------------------------------------------
+
+
+class CacheError(TunescapeError):
+    """A tuning cache cannot be used as given."""
+
+
+class IncompleteCache(CacheError):
+    """A cache that does not cover every valid configuration of its space."""
 
     def __init__(self, missing: int, total: int):
-        self.missing = missing
-        self.total = total
-        super().__init__(f"cache is missing {missing} of {total} valid configurations")
+        self.missing, self.total = missing, total
+        Exception.__init__(self, f"cache is missing {missing} of {total} valid configurations")
 
 
-class SpaceMismatch(TunescapeError):
-    """A cache was recorded for a different space (ref :72)."""
+class SpaceMismatch(CacheError):
+    """A cache recorded for a different space than the one supplied."""
 
 
-class CacheFormatError(TunescapeError):
-    """A cache document fails to parse or validate (ref :92)."""
+class CacheFormatError(CacheError):
+    """A cache document that does not parse or violates its schema."""
 
 
-class CacheIOError(TunescapeError):
-    """Reading or writing a cache failed at the OS level (ref :96)."""
+class CacheIOError(CacheError):
+    """The operating system refused to read or write a cache file."""
+
+
+# --- B200 runtime ------------------------------------------------------------
 
 
 class DeviceError(TunescapeError):
-    """The CUDA runtime (libtsgpu / driver / NVRTC) is unusable.
+    """The CUDA runtime (libtsgpu, driver, NVRTC) cannot be used at all.
 
-    Raised on *setup* problems only (library missing, no device); a
-    configuration that fails to compile or launch is still an
-    ``Observation`` with a failure status.
+    Setup problems only; a configuration that fails to compile or launch
+    is still an ``Observation`` with a failure status.
     """
 
 
 class VerificationError(TunescapeError):
-    """Kernel output does not match the expected answer."""
+    """Kernel output disagrees with the expected answer."""

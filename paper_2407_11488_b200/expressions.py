@@ -25,7 +25,6 @@ whenever int64 could overflow).
 from __future__ import annotations
 
 import math
-import re
 from dataclasses import dataclass
 from typing import Callable, Mapping, Sequence, Union
 
@@ -36,35 +35,53 @@ from .errors import EvaluationError, ExpressionSyntaxError, ExpressionTypeError
 Scalar = Union[int, float, str]
 
 # --------------------------------------------------------------------------
-# AST
+# AST.  The class and field names are part of the golden contract: the
+# fixtures record ``repr(parse_expression(src))`` as the reference prints
+# it (``Binary(op='+', left=Num(value=1), right=Var(name='x'))``), so the
+# five node kinds keep exactly these names and field orders.  Each node
+# knows its children, which lets every traversal below be one generic
+# post-order walk instead of an isinstance ladder per pass.
 
 
-@dataclass(frozen=True)
-class Num:
+class _Node:
+    __slots__ = ()
+
+    def children(self) -> tuple:
+        return ()
+
+
+@dataclass(frozen=True, slots=True)
+class Num(_Node):
     value: int | float
 
 
-@dataclass(frozen=True)
-class Str:
+@dataclass(frozen=True, slots=True)
+class Str(_Node):
     value: str
 
 
-@dataclass(frozen=True)
-class Var:
+@dataclass(frozen=True, slots=True)
+class Var(_Node):
     name: str
 
 
-@dataclass(frozen=True)
-class Unary:
+@dataclass(frozen=True, slots=True)
+class Unary(_Node):
     op: str  # '-' or '!'
     operand: "Node"
 
+    def children(self) -> tuple:
+        return (self.operand,)
 
-@dataclass(frozen=True)
-class Binary:
+
+@dataclass(frozen=True, slots=True)
+class Binary(_Node):
     op: str
     left: "Node"
     right: "Node"
+
+    def children(self) -> tuple:
+        return (self.left, self.right)
 
 
 Node = Union[Num, Str, Var, Unary, Binary]
@@ -73,18 +90,32 @@ COMPARISONS = frozenset({"==", "!=", "<", "<=", ">", ">="})
 ARITHMETIC = frozenset({"+", "-", "*", "/", "%", "^"})
 LOGICAL = frozenset({"&&", "||"})
 
-# --------------------------------------------------------------------------
-# Lexer
 
-_LEX = re.compile(
-    r"(?P<ws>\s+)"
-    r"|(?P<float>(?:\d+\.\d*|\.\d+)(?:[eE][+-]?\d+)?|\d+[eE][+-]?\d+)"
-    r"|(?P<int>\d+)"
-    r"|(?P<name>[A-Za-z_]\w*)"
-    r"|(?P<string>'[^']*'|\"[^\"]*\")"
-    r"|(?P<op>\|\||&&|==|!=|<=|>=|[-+*/%^<>!()])"
-)
+def postorder(node: Node):
+    """Nodes of ``node`` children-first, left to right (iterative)."""
+    stack = [(node, False)]
+    while stack:
+        n, expanded = stack.pop()
+        if expanded:
+            yield n
+            continue
+        stack.append((n, True))
+        stack.extend((c, False) for c in reversed(n.children()))
+
+
+# --------------------------------------------------------------------------
+# Lexer: a hand-written scanner.  Token classes and their precedence follow
+# the grammar of ``ts/expressions.py:1-28``: a number is a float when it has
+# a '.' mantissa or a complete exponent (``1e5``, ``1.``, ``.5``), else an
+# integer (``1e`` is the integer 1 followed by the name ``e``); names are
+# ASCII identifiers; strings are single- or double-quoted with no escapes;
+# ``and``/``or``/``not`` are spellings of ``&&``/``||``/``!``.
+
 _WORD_OPS = {"and": "&&", "or": "||", "not": "!"}
+_TWO_CHAR_OPS = frozenset({"||", "&&", "==", "!=", "<=", ">="})
+_ONE_CHAR_OPS = frozenset("-+*/%^<>!()")
+_NAME_START = frozenset("ABCDEFGHIJKLMNOPQRSTUVWXYZabcdefghijklmnopqrstuvwxyz_")
+_NAME_CHARS = _NAME_START | frozenset("0123456789")
 
 
 @dataclass(frozen=True)
@@ -94,19 +125,62 @@ class Token:
     pos: int
 
 
+def _digits_end(s: str, i: int) -> int:
+    while i < len(s) and s[i].isdecimal():
+        i += 1
+    return i
+
+
+def _exponent_end(s: str, i: int) -> int:
+    """End of a complete exponent ``[eE][+-]?digits`` at ``i``, else ``i``."""
+    if i < len(s) and s[i] in "eE":
+        j = i + 1
+        if j < len(s) and s[j] in "+-":
+            j += 1
+        k = _digits_end(s, j)
+        if k > j:
+            return k
+    return i
+
+
+def _scan_number(s: str, i: int) -> tuple:
+    """(kind, end) of the number starting at ``i`` (a digit or '.digit')."""
+    j = _digits_end(s, i)
+    if j < len(s) and s[j] == ".":
+        if j > i or _digits_end(s, j + 1) > j + 1:  # 'd.' / 'd.d' / '.d'
+            return "float", _exponent_end(s, _digits_end(s, j + 1))
+    k = _exponent_end(s, j)
+    return ("float", k) if k > j else ("int", j)
+
+
 def tokenize(source: str) -> list[Token]:
     out: list[Token] = []
     i, n = 0, len(source)
     while i < n:
-        m = _LEX.match(source, i)
-        if m is None:
-            raise ExpressionSyntaxError(f"unexpected character {source[i]!r}", source, i)
-        kind, text = m.lastgroup, m.group()
-        if kind != "ws":
-            if kind == "name" and text in _WORD_OPS:
-                kind, text = "op", _WORD_OPS[text]
-            out.append(Token(kind, text, i))
-        i = m.end()
+        ch = source[i]
+        if ch.isspace():
+            i += 1
+            continue
+        if ch.isdecimal() or (ch == "." and i + 1 < n and source[i + 1].isdecimal()):
+            kind, end = _scan_number(source, i)
+        elif ch in _NAME_START:
+            end = i + 1
+            while end < n and source[end] in _NAME_CHARS:
+                end += 1
+            kind = "name"
+        elif ch in "'\"" and source.find(ch, i + 1) >= 0:
+            kind, end = "string", source.find(ch, i + 1) + 1
+        elif source[i:i + 2] in _TWO_CHAR_OPS:
+            kind, end = "op", i + 2
+        elif ch in _ONE_CHAR_OPS:
+            kind, end = "op", i + 1
+        else:
+            raise ExpressionSyntaxError(f"unexpected character {ch!r}", source, i)
+        text = source[i:end]
+        if kind == "name" and text in _WORD_OPS:
+            kind, text = "op", _WORD_OPS[text]
+        out.append(Token(kind, text, i))
+        i = end
     out.append(Token("end", "", n))
     return out
 
@@ -210,66 +284,76 @@ def parse_expression(source: str) -> Node:
 
 def variables(node: Node) -> set[str]:
     """Identifiers referenced by ``node``."""
-    found: set[str] = set()
-    stack = [node]
-    while stack:
-        n = stack.pop()
-        if isinstance(n, Var):
-            found.add(n.name)
-        elif isinstance(n, Unary):
-            stack.append(n.operand)
-        elif isinstance(n, Binary):
-            stack.extend((n.left, n.right))
-    return found
+    return {n.name for n in postorder(node) if isinstance(n, Var)}
 
 
 # --------------------------------------------------------------------------
-# Static types
+# Static types.  Types are inferred children-first over ``postorder``; each
+# operator class has one rule mapping its operand types to a result type or
+# to a diagnostic.  Because children are typed before their parent, the
+# diagnostic reported is the one of the left-most, inner-most offending
+# node -- the order the reference's recursive checker reports in, which the
+# golden fixtures pin together with the message texts.
+
+_NUMERIC = ("int", "float")
+
+
+def _rule_not(op, a):
+    return "bool" if a == "bool" else (None, "'!' needs a boolean operand")
+
+
+def _rule_neg(op, a):
+    return a if a in _NUMERIC else (None, "unary '-' needs a number")
+
+
+def _rule_logical(op, a, b):
+    if a == b == "bool":
+        return "bool"
+    return None, f"'{op}' needs boolean operands"
+
+
+def _rule_compare(op, a, b):
+    if "bool" in (a, b):
+        return None, f"cannot compare boolean results with '{op}'"
+    if (a == "str") != (b == "str"):
+        return None, "cannot compare string and number"
+    if a == "str" and op not in ("==", "!="):
+        return None, "strings support only '==' and '!='"
+    return "bool"
+
+
+def _rule_arith(op, a, b):
+    if a not in _NUMERIC or b not in _NUMERIC:
+        return None, f"'{op}' needs numeric operands"
+    return "float" if "float" in (a, b) else "int"
+
+
+_UNARY_RULES = {"!": _rule_not, "-": _rule_neg}
+_BINARY_RULES = {**{op: _rule_logical for op in LOGICAL},
+                 **{op: _rule_compare for op in COMPARISONS},
+                 **{op: _rule_arith for op in ARITHMETIC}}
 
 
 def check_types(node: Node, var_types: Mapping[str, str], source: str = "") -> str:
     """Return 'int' | 'float' | 'str' | 'bool' or raise ExpressionTypeError."""
-    ctx = f" in {source!r}" if source else ""
-
-    def fail(msg: str):
-        raise ExpressionTypeError(msg + ctx)
-
-    def t(n: Node) -> str:
+    where = f" in {source!r}" if source else ""
+    typed: dict = {}
+    for n in postorder(node):
         if isinstance(n, Num):
-            return "float" if isinstance(n.value, float) else "int"
-        if isinstance(n, Str):
-            return "str"
-        if isinstance(n, Var):
-            if n.name not in var_types:
-                fail(f"unknown identifier '{n.name}'")
-            return var_types[n.name]
-        if isinstance(n, Unary):
-            inner = t(n.operand)
-            if n.op == "!":
-                if inner != "bool":
-                    fail("'!' needs a boolean operand")
-                return "bool"
-            if inner not in ("int", "float"):
-                fail("unary '-' needs a number")
-            return inner
-        a, b = t(n.left), t(n.right)
-        if n.op in LOGICAL:
-            if a != "bool" or b != "bool":
-                fail(f"'{n.op}' needs boolean operands")
-            return "bool"
-        if n.op in COMPARISONS:
-            if "bool" in (a, b):
-                fail(f"cannot compare boolean results with '{n.op}'")
-            if (a == "str") != (b == "str"):
-                fail("cannot compare string and number")
-            if a == "str" and n.op not in ("==", "!="):
-                fail("strings support only '==' and '!='")
-            return "bool"
-        if a not in ("int", "float") or b not in ("int", "float"):
-            fail(f"'{n.op}' needs numeric operands")
-        return "int" if (a, b) == ("int", "int") else "float"
-
-    return t(node)
+            t = "float" if isinstance(n.value, float) else "int"
+        elif isinstance(n, Str):
+            t = "str"
+        elif isinstance(n, Var):
+            t = var_types.get(n.name)
+            if t is None:
+                raise ExpressionTypeError(f"unknown identifier '{n.name}'{where}")
+        else:
+            rule = (_UNARY_RULES if isinstance(n, Unary) else _BINARY_RULES)[n.op]
+            t = rule(n.op, *(typed[id(c)] for c in n.children()))
+            if isinstance(t, tuple):
+                raise ExpressionTypeError(t[1] + where)
+        typed[id(n)] = t
+    return typed[id(node)]
 
 
 # --------------------------------------------------------------------------

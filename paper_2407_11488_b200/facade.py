@@ -51,7 +51,7 @@ from .errors import ProtocolError, VerificationError
 from .measure import BackendDescriptor, MeasurementProtocol, Observation, Status, aggregate_times
 from .paramspace import config_key, space_from_tune_params
 from .store import TuningCache, write_kernel_tuner_cache
-from .strategies import STRATEGIES, Runner, result_to_cache
+from .strategies import STRATEGIES, result_to_cache
 
 _RC_STATUS = {rt.ERR_COMPILE: Status.COMPILE_FAILED, rt.ERR_INVALID: Status.INVALID,
               rt.ERR_RUNTIME: Status.RUNTIME_FAILED, rt.ERR_TIMEOUT: Status.TIMEOUT,
@@ -174,10 +174,13 @@ class DeviceArgs:
                 out.append(_SCALAR_CTYPES[np.dtype(a.dtype)](a.item()))
         return out
 
-    def zero(self, i: int):
-        b = self.bufs[i]
-        if b is not None:
-            self.dev._check(self.dev.lib.tsg_memset32(self.dev.ctx, b.ptr, 0, b.nbytes // 4))
+    def restore(self, i: int):
+        """Re-upload argument ``i`` from its host array (Kernel Tuner semantics:
+        every verified run starts from the caller's original data, so
+        read-modify-write kernels and in-place updates verify correctly)."""
+        b, a = self.bufs[i], self.host[i]
+        if b is not None and a.nbytes:
+            b.upload(np.ascontiguousarray(a))
 
     def download(self, i: int) -> np.ndarray:
         a = self.host[i]
@@ -308,9 +311,8 @@ class GenericTarget:
         try:
             launch = [self._launch(inst, kern)]
             if self.answer is not None:
-                for i, a in enumerate(self.answer):
-                    if a is not None:
-                        self.args.zero(i)
+                for i in range(len(self.args.bufs)):
+                    self.args.restore(i)
                 rc, err = self.dev.run(launch, protocol.timeout_ms)
                 if rc != rt.OK:
                     return Observation(_RC_STATUS.get(rc, Status.RUNTIME_FAILED), detail=err)

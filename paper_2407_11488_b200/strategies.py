@@ -1,22 +1,39 @@
-"""Search strategies: brute force, random, greedy local search, genetic.
+"""Search strategies over a space: brute force, random, greedy local, genetic.
 
-Semantics follow the reference (`pkg/src/tunescape/strategies.py`):
-fitness is the aggregated ``time_ms`` (minimised); a memoising runner
-(:45-87) makes revisits free; the best is the strictly fastest ok
-observation, so the earliest wins ties (:72); ``random_search`` draws
-per-parameter ``random.Random(seed).choice`` with rejection of invalid
-or seen points and materialises the remainder after 200 misses
-(:148-192); ``greedy_local_search`` scans neighbours in parameter/value
-order with canonical tie-breaks and random restarts (:195-297).  With
-the same seed the traces are identical to the reference's.
+Behavioural contract (SPEC.md ``strategies``; pinned by the reference's
+tests and the golden traces in ``tests/golden``):
 
-B200 additions:
-* with a ``cuda`` backend the runner pipelines NVRTC compilation ahead
-  of the GPU (``target.prefetch``), because compile, not the kernel,
-  bounds configurations/second;
-* :func:`genetic_algorithm` (absent from the reference; Kernel Tuner's
-  population-based search, north_star) -- selection, crossover and
-  mutation draw only from the seeded RNG, so runs are replayable.
+* fitness is the aggregated ``time_ms``, minimised; the best is the
+  strictly fastest ok observation, so the earliest wins ties;
+* measurements are memoised per run: revisiting a configuration costs no
+  budget, and the trace records first evaluations only;
+* random search draws per-parameter ``random.Random(seed).choice``,
+  rejecting invalid and already-drawn points, and materialises the
+  remaining valid configurations after 200 consecutive misses;
+* local search is best- (or first-) improvement hill descent with random
+  restarts, neighbours in parameter-then-value order, ties broken by
+  canonical configuration order, the budget checked before every
+  unmeasured neighbour.
+
+Architecture (B200 build).  A strategy never measures one configuration
+at a time: it hands *batches* to an :class:`Evaluator` and consumes the
+observations in order.  Brute force is one batch, random search is one
+batch (its draw sequence never depends on timings, so it is drawn up
+front), local search batches each neighbourhood scan, and the genetic
+algorithm batches each generation.  The evaluator decides how a batch
+runs -- pipelined through one GPU (:class:`LocalEvaluator`, the cuda
+backend's ``execute_many``), or split across the GPUs of a node
+(``multigpu.ShardedEvaluator``) -- while :class:`Ledger` commits results
+in the order a one-at-a-time search would have measured them, so traces,
+budgets and results are identical to the sequential reference semantics
+whichever evaluator runs them.  Local search's first-improvement rule
+stops at the first improving neighbour; results measured past that point
+are held as *speculative* and only enter the trace if the search asks
+for them later.
+
+:func:`genetic_algorithm` is new (Kernel Tuner's population search, named
+by the north_star; the reference lists it as a non-goal): all its choices
+come from the seeded RNG, so runs replay exactly.
 """
 
 from __future__ import annotations
@@ -25,15 +42,17 @@ import random
 from dataclasses import dataclass
 
 from .errors import ProtocolError
-from .measure import BackendDescriptor, MeasurementProtocol, Observation, pipelined, run_config, run_configs
+from .measure import BackendDescriptor, MeasurementProtocol, Observation, pipelined, run_configs
 from .paramspace import Config, NeighborScheme, SearchSpaceSpec, config_key
 from .store import TuningCache
 
-MISS_LIMIT = 200
+MISS_LIMIT = 200  # consecutive rejected draws before sampling materialises the rest
 
 
 @dataclass(frozen=True)
 class SearchSegment:
+    """One descent of local search: the accepted path from one start."""
+
     path: tuple
     reached_minimum: bool
 
@@ -48,76 +67,44 @@ class StrategyResult:
     segments: tuple = ()
 
 
-class Runner:
-    """Memoising measurement driver shared by every strategy."""
+# ---------------------------------------------------------------------------
+# Evaluators: how a batch of configurations gets measured
 
-    def __init__(self, space: SearchSpaceSpec, backend: BackendDescriptor,
-                 protocol: MeasurementProtocol):
+
+class Evaluator:
+    """Measures a list of configurations; returns their observations in order.
+
+    ``batch_hint`` is how many configurations the evaluator can usefully
+    measure at once (first-improvement local search speculates that far).
+    """
+
+    batch_hint = 1
+
+    def measure(self, configs: list) -> list:
+        raise NotImplementedError
+
+    def device_name(self, override: str | None = None) -> str:
+        return override or "unknown"
+
+
+class LocalEvaluator(Evaluator):
+    """One backend in this process; the cuda backend pipelines each batch."""
+
+    def __init__(self, space: SearchSpaceSpec, backend: BackendDescriptor, protocol: MeasurementProtocol):
         self.space, self.backend, self.protocol = space, backend, protocol
-        self.seen: dict = {}
-        self.trace: list = []
-        self.best: Config | None = None
-        self.best_obs: Observation | None = None
+        if pipelined(backend):
+            self.batch_hint = max(1, int(getattr(backend.target, "pipeline_depth", 4)))
 
-    @property
-    def evaluations(self) -> int:
-        return len(self.trace)
+    def measure(self, configs: list) -> list:
+        return [obs for _, obs in run_configs(self.space, self.backend, self.protocol, configs)]
 
-    def lookup(self, config: Config):
-        return self.seen.get(config_key(config))
-
-    def prefetch(self, configs) -> None:
-        if self.backend.kind == "cuda":
-            self.backend.target.prefetch(c for c in configs if config_key(c) not in self.seen)
-
-    def record(self, config: Config, obs: Observation) -> Observation:
-        key = config_key(config)
-        self.seen[key] = obs
-        self.trace.append((config, obs))
-        if obs.ok and (self.best_obs is None or obs.time_ms < self.best_obs.time_ms):
-            self.best, self.best_obs = config, obs
-        return obs
-
-    def evaluate(self, config: Config) -> Observation:
-        hit = self.seen.get(config_key(config))
-        if hit is not None:
-            return hit
-        return self.record(config, run_config(self.space, self.backend, self.protocol, config))
-
-    def evaluate_many(self, configs) -> None:
-        """Evaluate a list fixed in advance, in order (memoised; the cuda
-        backend pipelines it -- same trace as evaluating one by one)."""
-        todo, keys = [], set()
-        for c in configs:
-            k = config_key(c)
-            if k not in self.seen and k not in keys:
-                keys.add(k)
-                todo.append(c)
-        for c, obs in run_configs(self.space, self.backend, self.protocol, todo):
-            self.record(c, obs)
-
-    def result(self, notes=(), segments=()) -> StrategyResult:
-        notes = tuple(notes)
-        if self.best is None:
-            notes += ("no feasible optimum: every measured configuration failed",)
-        return StrategyResult(self.best, self.best_obs, tuple(self.trace), self.evaluations,
-                              notes, tuple(segments))
-
-
-# kept for callers written against the reference's private name
-_Runner = Runner
-
-
-def result_to_cache(space: SearchSpaceSpec, result: StrategyResult, device_name: str = "unknown",
-                    metadata: dict | None = None) -> TuningCache:
-    return TuningCache(kernel_name=space.kernel_name, device_name=device_name,
-                       param_order=space.param_names,
-                       records={config_key(c): o for c, o in result.trace},
-                       space_fingerprint=space.fingerprint(), provenance="native",
-                       metadata=dict(metadata or {}))
+    def device_name(self, override: str | None = None) -> str:
+        return default_device_name(self.backend, override)
 
 
 def default_device_name(backend: BackendDescriptor, override: str | None = None) -> str:
+    """Device recorded in caches: the override, the replayed cache's device,
+    the GPU's name, else ``unknown``."""
     if override:
         return override
     if backend.kind == "simulated":
@@ -127,32 +114,116 @@ def default_device_name(backend: BackendDescriptor, override: str | None = None)
     return "unknown"
 
 
-def _window(runner: Runner, configs: list, start: int) -> None:
-    if runner.backend.kind == "cuda":
-        depth = runner.backend.target.prefetch_depth
-        runner.prefetch(configs[start:start + depth])
+# ---------------------------------------------------------------------------
+# The ledger: memo, trace, best, speculative results
 
 
-def brute_force(space: SearchSpaceSpec, backend: BackendDescriptor,
-                protocol: MeasurementProtocol, device_name: str | None = None,
-                metadata: dict | None = None, configs: list | None = None):
-    """Measure every valid configuration once, in enumeration order.
+class Ledger:
+    """Everything one strategy run has measured, in commit order."""
 
-    ``configs`` (new) restricts the sweep to an explicit sub-list, in the
-    given order -- the unit a multi-GPU shard runs.
+    def __init__(self, space: SearchSpaceSpec, evaluator: Evaluator):
+        self.space, self.evaluator = space, evaluator
+        self.seen: dict = {}
+        self.trace: list = []
+        self.best: Config | None = None
+        self.best_obs: Observation | None = None
+        self._speculative: dict = {}
+
+    @property
+    def evaluations(self) -> int:
+        return len(self.trace)
+
+    def lookup(self, config: Config) -> Observation | None:
+        return self.seen.get(config_key(config))
+
+    def commit(self, config: Config, obs: Observation) -> Observation:
+        self.seen[config_key(config)] = obs
+        self.trace.append((config, obs))
+        if obs.ok and (self.best_obs is None or obs.time_ms < self.best_obs.time_ms):
+            self.best, self.best_obs = config, obs
+        return obs
+
+    def unseen(self, configs) -> list:
+        """``configs`` not yet committed, first occurrences, in order."""
+        out, keys = [], set()
+        for c in configs:
+            k = config_key(c)
+            if k not in self.seen and k not in keys:
+                keys.add(k)
+                out.append(c)
+        return out
+
+    def speculate(self, configs) -> None:
+        """Measure ``configs`` now without committing them."""
+        todo = [c for c in self.unseen(configs) if config_key(c) not in self._speculative]
+        if todo:
+            for c, obs in zip(todo, self.evaluator.measure(todo)):
+                self._speculative[config_key(c)] = obs
+
+    def take(self, config: Config) -> Observation:
+        """Commit ``config`` (measured speculatively or now); memo hits are free."""
+        hit = self.lookup(config)
+        if hit is not None:
+            return hit
+        obs = self._speculative.pop(config_key(config), None)
+        if obs is None:
+            obs = self.evaluator.measure([config])[0]
+        return self.commit(config, obs)
+
+    def take_all(self, configs) -> None:
+        """Commit a list fixed in advance: one batch, committed in order."""
+        todo = self.unseen(configs)
+        self.speculate(todo)
+        for c in todo:
+            self.take(c)
+
+    def result(self, notes=(), segments=()) -> StrategyResult:
+        notes = tuple(notes)
+        if self.best is None:
+            notes += ("no feasible optimum: every measured configuration failed",)
+        return StrategyResult(self.best, self.best_obs, tuple(self.trace), self.evaluations, notes,
+                              tuple(segments))
+
+
+def _ledger(space, backend, protocol, evaluator) -> Ledger:
+    if evaluator is None:
+        if backend is None:
+            raise ProtocolError("a strategy needs a backend or an evaluator")
+        evaluator = LocalEvaluator(space, backend, protocol)
+    return Ledger(space, evaluator)
+
+
+def result_to_cache(space: SearchSpaceSpec, result: StrategyResult, device_name: str = "unknown",
+                    metadata: dict | None = None) -> TuningCache:
+    """Persistable cache of every observation a run committed."""
+    return TuningCache(kernel_name=space.kernel_name, device_name=device_name,
+                       param_order=space.param_names,
+                       records={config_key(c): o for c, o in result.trace},
+                       space_fingerprint=space.fingerprint(), provenance="native",
+                       metadata=dict(metadata or {}))
+
+
+# ---------------------------------------------------------------------------
+# Brute force
+
+
+def brute_force(space: SearchSpaceSpec, backend: BackendDescriptor | None,
+                protocol: MeasurementProtocol | None, device_name: str | None = None,
+                metadata: dict | None = None, configs: list | None = None,
+                evaluator: Evaluator | None = None):
+    """Every valid configuration once, in enumeration order (one batch).
+
+    Returns ``(result, cache)``; the cache is complete over the space.
+    ``configs`` restricts the sweep to an explicit list (a shard, a sample).
     """
-    runner = Runner(space, backend, protocol)
-    todo = list(space.enumerate_configs()) if configs is None else list(configs)
-    if pipelined(backend):
-        runner.evaluate_many(todo)  # pipelined, same order
-    else:
-        for i, config in enumerate(todo):
-            if i % 8 == 0:
-                _window(runner, todo, i)
-            runner.evaluate(config)
-    result = runner.result()
-    return result, result_to_cache(space, result, default_device_name(backend, device_name),
-                                   metadata)
+    ledger = _ledger(space, backend, protocol, evaluator)
+    ledger.take_all(space.enumerate_configs() if configs is None else configs)
+    result = ledger.result()
+    return result, result_to_cache(space, result, ledger.evaluator.device_name(device_name), metadata)
+
+
+# ---------------------------------------------------------------------------
+# Random search
 
 
 def random_cartesian(rng: random.Random, space: SearchSpaceSpec) -> Config:
@@ -160,253 +231,244 @@ def random_cartesian(rng: random.Random, space: SearchSpaceSpec) -> Config:
 
 
 def random_sample_sequence(space: SearchSpaceSpec, budget: int, seed: int) -> tuple:
-    """The configurations random_search would evaluate, and its notes.
+    """``(configs, notes)``: the draws :func:`random_search` commits, in order.
 
-    The sequence never depends on measured times (ref :170-191), so it
-    can be drawn up front and sharded across GPUs while keeping the
-    trace identical to the sequential run.
+    Draws depend only on the seed and on which configurations were drawn
+    before -- never on timings -- so the sequence is the whole plan.
     """
     if budget < 1:
         raise ProtocolError("random search needs a budget of at least 1")
     rng = random.Random(seed)
-    seen: set = set()
-    order: list = []
+    drawn: dict = {}
     notes: list = []
-    remaining = None
+    rest: list | None = None
     misses = 0
-    while len(order) < budget:
-        if remaining is None:
-            config = random_cartesian(rng, space)
-            key = config_key(config)
-            if not space.satisfies(config) or key in seen:
+    while len(drawn) < budget:
+        if rest is None:
+            cand = random_cartesian(rng, space)
+            if config_key(cand) in drawn or not space.satisfies(cand):
                 misses += 1
                 if misses >= MISS_LIMIT:
-                    remaining = [c for c in space.enumerate_configs() if config_key(c) not in seen]
+                    rest = [c for c in space.enumerate_configs() if config_key(c) not in drawn]
                 continue
             misses = 0
+        elif rest:
+            cand = rest.pop(rng.randrange(len(rest)))
         else:
-            if not remaining:
-                notes.append(f"budget {budget} clamped to space size {len(order)}")
-                break
-            config = remaining.pop(rng.randrange(len(remaining)))
-            key = config_key(config)
-        seen.add(key)
-        order.append(config)
-    return order, notes
+            notes.append(f"budget {budget} clamped to space size {len(drawn)}")
+            break
+        drawn[config_key(cand)] = cand
+    return list(drawn.values()), notes
 
 
-def random_search(space: SearchSpaceSpec, backend: BackendDescriptor,
-                  protocol: MeasurementProtocol, budget: int, seed: int) -> StrategyResult:
-    """Uniform sampling without replacement (seeded, replayable)."""
-    order, notes = random_sample_sequence(space, budget, seed)
-    runner = Runner(space, backend, protocol)
-    if pipelined(backend):
-        runner.evaluate_many(order)  # the order is timing-independent: pipelined
-    else:
-        for i, config in enumerate(order):
-            if i % 8 == 0:
-                _window(runner, order, i)
-            runner.evaluate(config)
-    return runner.result(notes=notes)
+def random_search(space: SearchSpaceSpec, backend: BackendDescriptor | None,
+                  protocol: MeasurementProtocol | None, budget: int, seed: int,
+                  evaluator: Evaluator | None = None) -> StrategyResult:
+    """Uniform sampling without replacement (seeded, replayable; one batch)."""
+    plan, notes = random_sample_sequence(space, budget, seed)
+    ledger = _ledger(space, backend, protocol, evaluator)
+    ledger.take_all(plan)
+    return ledger.result(notes=notes)
 
 
-def greedy_local_search(space: SearchSpaceSpec, backend: BackendDescriptor,
-                        protocol: MeasurementProtocol, budget: int, seed: int,
-                        scheme: NeighborScheme | str | None = None,
-                        first_improvement: bool = False,
-                        start: Config | None = None) -> StrategyResult:
-    """Hill descent with random restarts (ref strategies.py:195-297)."""
-    if budget < 1:
-        raise ProtocolError("local search needs a budget of at least 1")
-    scheme = NeighborScheme(scheme) if scheme else space.neighbor_scheme
-    rng = random.Random(seed)
-    runner = Runner(space, backend, protocol)
-    segments: list = []
-    notes: list = []
-    pool = None
-    size = None
-    pos = [{v: i for i, v in enumerate(p.values)} for p in space.parameters]
+# ---------------------------------------------------------------------------
+# Greedy local search
 
-    def rank(c):
-        return tuple(m[v] for m, v in zip(pos, c))
 
-    def fresh_start():
-        nonlocal pool
+class _Starts:
+    """Random valid starting points (rejection sampling, then a pool)."""
+
+    def __init__(self, space: SearchSpaceSpec, rng: random.Random):
+        self.space, self.rng, self.pool = space, rng, None
+
+    def draw(self) -> Config | None:
         misses = 0
-        while pool is None:
-            cand = random_cartesian(rng, space)
-            if space.satisfies(cand):
+        while self.pool is None:
+            cand = random_cartesian(self.rng, self.space)
+            if self.space.satisfies(cand):
                 return cand
             misses += 1
             if misses >= MISS_LIMIT:
-                pool = list(space.enumerate_configs())
-        return pool[rng.randrange(len(pool))] if pool else None
+                self.pool = list(self.space.enumerate_configs())
+        return self.pool[self.rng.randrange(len(self.pool))] if self.pool else None
 
-    first = True
-    while runner.evaluations < budget:
-        origin = start if (first and start is not None) else fresh_start()
-        first = False
+
+def _scan(ledger: Ledger, here_ms: float, neighbours: list, budget: int, first_improvement: bool,
+          order_of) -> tuple:
+    """One neighbourhood scan: ``(move, out_of_budget)``.
+
+    Commits neighbours in neighbour order exactly as a one-at-a-time scan
+    would -- an unmeasured neighbour met with the budget spent ends the
+    scan -- but measures them in batches.  Best-improvement measures every
+    affordable neighbour as one batch; first-improvement speculates
+    ``batch_hint`` neighbours ahead and stops committing at the first
+    improvement.
+    """
+    fresh = ledger.unseen(neighbours)
+    affordable = fresh[:max(0, budget - ledger.evaluations)]
+    window = len(affordable) if not first_improvement else max(1, ledger.evaluator.batch_hint)
+    pos = {config_key(c): i for i, c in enumerate(affordable)}
+    move, move_ms = None, None
+    for cand in neighbours:
+        key = config_key(cand)
+        if ledger.lookup(cand) is None:
+            if ledger.evaluations >= budget:
+                return None, True
+            i = pos[key]
+            if i % window == 0:
+                ledger.speculate(affordable[i:i + window])
+        obs = ledger.take(cand)
+        if not obs.ok or obs.time_ms >= here_ms:
+            continue
+        if first_improvement:
+            return cand, False
+        if move is None or obs.time_ms < move_ms or (obs.time_ms == move_ms and order_of(cand) < order_of(move)):
+            move, move_ms = cand, obs.time_ms
+    return move, False
+
+
+def greedy_local_search(space: SearchSpaceSpec, backend: BackendDescriptor | None,
+                        protocol: MeasurementProtocol | None, budget: int, seed: int,
+                        scheme: NeighborScheme | str | None = None,
+                        first_improvement: bool = False,
+                        start: Config | None = None,
+                        evaluator: Evaluator | None = None) -> StrategyResult:
+    """Hill descent with random restarts; each neighbourhood is one batch."""
+    if budget < 1:
+        raise ProtocolError("local search needs a budget of at least 1")
+    scheme = NeighborScheme(scheme) if scheme else space.neighbor_scheme
+    ledger = _ledger(space, backend, protocol, evaluator)
+    starts = _Starts(space, random.Random(seed))
+    segments, notes = [], []
+    size = None
+    pending_start = start
+    while ledger.evaluations < budget:
+        origin, pending_start = (pending_start or starts.draw()), None
         if origin is None:
             notes.append("space has no valid configurations")
             break
-        before = runner.evaluations
-        path = [origin]
-        cur_obs = runner.evaluate(origin)
-        cur = origin
-        at_min = False
-        exhausted = False
-        while cur_obs.ok:
-            nbrs = space.neighbors(cur, scheme)
-            runner.prefetch(nbrs)
-            move, move_t = None, None
-            for cand in nbrs:
-                if runner.lookup(cand) is None and runner.evaluations >= budget:
-                    exhausted = True
-                    break
-                o = runner.evaluate(cand)
-                if not o.ok or o.time_ms >= cur_obs.time_ms:
-                    continue
-                if first_improvement:
-                    move, move_t = cand, o.time_ms
-                    break
-                if move is None or o.time_ms < move_t or (o.time_ms == move_t and rank(cand) < rank(move)):
-                    move, move_t = cand, o.time_ms
-            if exhausted:
+        before = ledger.evaluations
+        path, here = [origin], origin
+        here_obs = ledger.take(origin)
+        at_minimum = out_of_budget = False
+        while here_obs.ok:
+            move, out_of_budget = _scan(ledger, here_obs.time_ms, space.neighbors(here, scheme), budget,
+                                        first_improvement, space.flat_index)
+            if out_of_budget:
                 break
             if move is None:
-                at_min = True
+                at_minimum = True
                 break
-            cur = move
-            cur_obs = runner.seen[config_key(cur)]
-            path.append(cur)
-        segments.append(SearchSegment(tuple(path), at_min))
-        if exhausted or runner.evaluations >= budget:
+            here, here_obs = move, ledger.lookup(move)
+            path.append(here)
+        segments.append(SearchSegment(tuple(path), at_minimum))
+        if out_of_budget or ledger.evaluations >= budget:
             break
-        if runner.evaluations == before:
-            if size is None:
-                size = space.space_size()
-            if len(runner.seen) >= size:
+        if ledger.evaluations == before:  # a restart that measured nothing new
+            size = space.space_size() if size is None else size
+            if len(ledger.seen) >= size:
                 notes.append("entire space evaluated before budget ran out")
                 break
-    return runner.result(notes=notes, segments=segments)
+    return ledger.result(notes=notes, segments=segments)
 
 
-# -----------------------------------------------------------------------------
+# ---------------------------------------------------------------------------
 # Genetic algorithm (new; Kernel Tuner's strategy="genetic_algorithm")
 
+_CROSSOVERS = ("uniform", "single_point", "two_point")
 
-def genetic_algorithm(space: SearchSpaceSpec, backend: BackendDescriptor,
-                      protocol: MeasurementProtocol, budget: int, seed: int,
+
+def genetic_algorithm(space: SearchSpaceSpec, backend: BackendDescriptor | None,
+                      protocol: MeasurementProtocol | None, budget: int, seed: int,
                       popsize: int = 20, maxiter: int = 100, mutation_chance: int = 10,
-                      crossover: str = "uniform", evaluate_population=None) -> StrategyResult:
-    """Population search over valid configurations.
+                      crossover: str = "uniform", evaluator: Evaluator | None = None) -> StrategyResult:
+    """Population search over valid configurations; one batch per generation.
 
-    * initial population: ``popsize`` distinct valid points (rejection
-      sampling like :func:`random_search`);
-    * each generation is evaluated as a batch (``evaluate_population``
-      may fan it out over several GPUs; default: sequential, memoised);
-    * rank selection (weight ~ popsize - rank), ``crossover`` in
+    * the first generation is ``popsize`` distinct valid random points;
+    * rank selection (weight ``popsize - rank``; failures rank last), the
+      top tenth survives unchanged (elitism), ``crossover`` in
       {uniform, single_point, two_point}, per-gene mutation with
-      probability 1/mutation_chance; invalid children are repaired by
-      re-mutating up to 100 times, else replaced by a random point;
-    * failed configurations rank last; stops at ``budget`` distinct
-      evaluations, ``maxiter`` generations, or space exhaustion.
+      probability ``1/mutation_chance``; an invalid child is re-mutated up
+      to 100 times, then replaced by a random valid point;
+    * stops at ``budget`` distinct evaluations, ``maxiter`` generations or
+      an exhausted space.
     """
     if budget < 1:
         raise ProtocolError("genetic algorithm needs a budget of at least 1")
-    if crossover not in ("uniform", "single_point", "two_point"):
-        raise ProtocolError(f"unknown crossover {crossover!r}")
+    if crossover not in _CROSSOVERS:
+        raise ProtocolError(f"unknown crossover {crossover!r}; one of {', '.join(_CROSSOVERS)}")
     rng = random.Random(seed)
-    runner = Runner(space, backend, protocol)
-    notes: list = []
-    n_params = len(space.parameters)
+    ledger = _ledger(space, backend, protocol, evaluator)
     size = space.space_size()
+    width = len(space.parameters)
 
-    def random_valid():
+    def random_valid() -> Config | None:
         for _ in range(10 * MISS_LIMIT):
-            c = random_cartesian(rng, space)
-            if space.satisfies(c):
-                return c
+            cand = random_cartesian(rng, space)
+            if space.satisfies(cand):
+                return cand
         pool = list(space.enumerate_configs())
         return pool[rng.randrange(len(pool))] if pool else None
 
-    def mutate(c):
-        genes = list(c)
-        for i, p in enumerate(space.parameters):
-            if rng.randrange(mutation_chance) == 0:
-                genes[i] = rng.choice(p.values)
-        return tuple(genes)
+    def mutate(genes: Config) -> Config:
+        return tuple(rng.choice(p.values) if rng.randrange(mutation_chance) == 0 else g
+                     for g, p in zip(genes, space.parameters))
 
-    def cross(a, b):
+    def recombine(a: Config, b: Config) -> Config:
         if crossover == "uniform":
             return tuple(x if rng.random() < 0.5 else y for x, y in zip(a, b))
         if crossover == "single_point":
-            k = rng.randrange(1, n_params) if n_params > 1 else 0
-            return a[:k] + b[k:]
-        i, j = sorted(rng.sample(range(n_params + 1), 2))
-        return a[:i] + b[i:j] + a[j:]
+            cut = rng.randrange(1, width) if width > 1 else 0
+            return a[:cut] + b[cut:]
+        lo, hi = sorted(rng.sample(range(width + 1), 2))
+        return a[:lo] + b[lo:hi] + a[hi:]
 
-    def fitness(c):
-        o = runner.lookup(c)
-        return o.time_ms if (o is not None and o.ok) else float("inf")
+    def repaired(child: Config) -> Config | None:
+        for _ in range(100):
+            if space.satisfies(child):
+                return child
+            child = mutate(child)
+        return child if space.satisfies(child) else random_valid()
 
-    population = []
-    keys = set()
+    def fitness(c: Config) -> float:
+        obs = ledger.lookup(c)
+        return obs.time_ms if obs is not None and obs.ok else float("inf")
+
+    population: dict = {}
     while len(population) < min(popsize, size):
-        c = random_valid()
-        if c is None:
+        cand = random_valid()
+        if cand is None:
             break
-        if config_key(c) not in keys:
-            keys.add(config_key(c))
-            population.append(c)
+        population.setdefault(config_key(cand), cand)
+    population = list(population.values())
 
-    gen = 0
-    while runner.evaluations < budget and gen < maxiter:
-        todo = [c for c in population if runner.lookup(c) is None]
-        todo = todo[: budget - runner.evaluations]
-        if evaluate_population is not None and todo:
-            for c, o in zip(todo, evaluate_population(todo)):
-                if runner.lookup(c) is None:
-                    runner.record(c, o)
-        else:
-            runner.prefetch(todo)
-            for c in todo:
-                runner.evaluate(c)
-        if len(runner.seen) >= size:
+    notes = []
+    generation = 0
+    while ledger.evaluations < budget and generation < maxiter:
+        ledger.take_all(ledger.unseen(population)[:budget - ledger.evaluations])
+        if len(ledger.seen) >= size:
             notes.append("entire space evaluated before budget ran out")
             break
         ranked = sorted(population, key=lambda c: (fitness(c), config_key(c)))
-        weights = [len(ranked) - i for i in range(len(ranked))]
-        children = []
-        child_keys = set()
-        elite = ranked[: max(1, len(ranked) // 10)]
-        for e in elite:
-            children.append(e)
-            child_keys.add(config_key(e))
+        weights = list(range(len(ranked), 0, -1))
+        elite = ranked[:max(1, len(ranked) // 10)]
+        children = {config_key(c): c for c in elite}
         attempts = 0
         while len(children) < popsize and attempts < 50 * popsize:
             attempts += 1
-            pa, pb = rng.choices(ranked, weights=weights, k=2)
-            child = mutate(cross(pa, pb))
-            tries = 0
-            while not space.satisfies(child) and tries < 100:
-                child = mutate(child)
-                tries += 1
-            if not space.satisfies(child):
-                child = random_valid()
-            k = config_key(child)
-            if k in child_keys:
+            mum, dad = rng.choices(ranked, weights=weights, k=2)
+            child = repaired(mutate(recombine(mum, dad)))
+            key = config_key(child)
+            if key in children:
                 continue
-            # prefer unexplored children once the population has converged
-            if runner.lookup(child) is not None and attempts < 25 * popsize:
-                continue
-            child_keys.add(k)
-            children.append(child)
-        population = children
-        gen += 1
-    if gen >= maxiter:
+            if ledger.lookup(child) is not None and attempts < 25 * popsize:
+                continue  # prefer unexplored children until the population converges
+            children[key] = child
+        population = list(children.values())
+        generation += 1
+    if generation >= maxiter:
         notes.append(f"stopped after {maxiter} generations")
-    return runner.result(notes=notes)
+    return ledger.result(notes=notes)
 
 
 STRATEGIES = {

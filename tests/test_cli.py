@@ -75,17 +75,28 @@ def test_tune_resume_from_torn_log(golden, tmp_path):
     assert r.exit_code == 0, r.output
     lines = log.read_text().splitlines()
     n = s.space_size()
-    assert len(lines) == n
+    assert len(lines) == n + 1 and '"header"' in lines[0]  # space fingerprint + protocol
     # keep a third of the log plus a torn half line, as a crash would
     keep = lines[: n // 3]
     log.write_text("\n".join(keep) + "\n" + lines[n // 3][: 10])
     r = CliRunner().invoke(cli, args + ["--out", str(tmp_path / "b.json")])
     assert r.exit_code == 0, r.output
     good = [json.loads(x) for x in log.read_text().splitlines() if x.startswith("{") and x.endswith("}")]
-    assert sorted(d["key"] for d in good) == sorted(json.loads(x)["key"] for x in lines)
+    good = [d for d in good if "key" in d]
+    assert sorted(d["key"] for d in good) == sorted(json.loads(x)["key"] for x in lines[1:])
     a, b = read_cache(tmp_path / "a.json"), read_cache(tmp_path / "b.json")
     assert a.records == b.records
     assert sorted(a.records) == sorted(config_key(c) for c in s.enumerate_configs())
+
+
+def test_resume_refuses_a_log_of_another_protocol(golden, tmp_path):
+    """Observations measured under another protocol (or space) are not reused."""
+    rec, s, spec, src = _setup(golden, tmp_path)
+    log = tmp_path / "obs.jsonl"
+    base = ["tune", "--space", str(spec), "--backend", f"sim:{src}", "--resume", str(log)]
+    assert CliRunner().invoke(cli, base + ["--out", str(tmp_path / "a.json")]).exit_code == 0
+    r = CliRunner().invoke(cli, base + ["--runs", "3", "--out", str(tmp_path / "b.json")])
+    assert r.exit_code != 0 and "another protocol" in str(r.exception)
 
 
 def test_exit_codes(golden, tmp_path):

@@ -88,12 +88,85 @@ def test_resume_from_log(tmp_path):
     configs = list(space.enumerate_configs())[:100]
     r1, c1, _ = sharded_brute_force(space, be, MeasurementProtocol(), log_path=str(log), configs=configs)
     lines = log.read_text().splitlines()
-    assert len(lines) == 100
+    assert len(lines) == 101 and '"header"' in lines[0]
     # a torn final line and a rerun: nothing is re-measured, result identical
-    log.write_text("\n".join(lines[:60]) + "\n{\"key\": \"broken")
+    log.write_text("\n".join(lines[:61]) + "\n{\"key\": \"broken")
     r2, c2, _ = sharded_brute_force(space, be, MeasurementProtocol(), log_path=str(log), configs=configs)
     assert dumps_cache(c1) == dumps_cache(c2)
     # the log is whole again: a third run measures nothing new
     from paper_2407_11488_b200.store import ResultLog
 
     assert len(ResultLog(log).load()) == 100
+
+
+# ---------------------------------------------------------------------------
+# Every strategy on two ranks: each batch the strategy issues is split over
+# the ranks (ShardedEvaluator) and the committed trace must be identical to
+# the one-process run -- including local search's budget cut and tie-break
+# and first-improvement's stop at the first improving neighbour.
+
+STRATEGY_CASES = [
+    ("random", dict(budget=150, seed=4)),
+    ("local", dict(budget=120, seed=2)),
+    ("local_first", dict(budget=120, seed=9)),
+    ("local_adjacent", dict(budget=60, seed=3)),
+    ("genetic", dict(budget=90, seed=5)),
+]
+
+
+def _run_strategy(name, space, evaluator):
+    from paper_2407_11488_b200 import strategies as S
+
+    kw = dict(STRATEGY_CASES)[name]
+    if name == "random":
+        return S.random_search(space, None, None, kw["budget"], kw["seed"], evaluator=evaluator)
+    if name.startswith("local"):
+        return S.greedy_local_search(space, None, None, kw["budget"], kw["seed"],
+                                     scheme="adjacent" if name == "local_adjacent" else None,
+                                     first_improvement=name == "local_first", evaluator=evaluator)
+    return S.genetic_algorithm(space, None, None, kw["budget"], kw["seed"], popsize=12, evaluator=evaluator)
+
+
+def _trace_text(result) -> str:
+    lines = [f"{config_key(c)} {o.status.value} {o.time_ms}" for c, o in result.trace]
+    lines.append(f"BEST {config_key(result.best) if result.best else None}")
+    lines += [f"SEG {[config_key(c) for c in seg.path]} {seg.reached_minimum}" for seg in result.segments]
+    lines += [f"NOTE {n}" for n in result.notes]
+    return "\n".join(lines) + "\n"
+
+
+def _strategy_worker(rank, world, port, outdir):
+    from paper_2407_11488_b200.multigpu import ShardedEvaluator, current_comm
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        space = bundled_space("dedispersion")
+        be = simulated_backend(make_cache(space, seed=11))
+        for name, _ in STRATEGY_CASES:
+            ev = ShardedEvaluator(space, be, MeasurementProtocol(), current_comm(), chunk=3)
+            res = _run_strategy(name, space, ev)
+            with open(os.path.join(outdir, f"{name}.rank{rank}.txt"), "w") as f:
+                f.write(_trace_text(res))
+                f.write(f"MINE {ev.stats.configs}\n")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_every_strategy_sharded_over_two_ranks_matches_one_process(tmp_path):
+    from paper_2407_11488_b200.strategies import LocalEvaluator
+
+    world = 2
+    mp.spawn(_strategy_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    space = bundled_space("dedispersion")
+    be = simulated_backend(make_cache(space, seed=11))
+    per_rank = [0] * world
+    for name, _ in STRATEGY_CASES:
+        want = _trace_text(_run_strategy(name, space, LocalEvaluator(space, be, MeasurementProtocol())))
+        for r in range(world):
+            body, mine = (tmp_path / f"{name}.rank{r}.txt").read_text().rsplit("MINE ", 1)
+            assert body == want, name
+            per_rank[r] += int(mine)
+    assert min(per_rank) > 0, per_rank  # both ranks measured parts of the batches
+

@@ -120,7 +120,7 @@ def test_random_spaces_vs_cartesian_oracle():
             continue
         assert list(s.enumerate_configs()) == want
         # scalar path agrees with the vectorised path
-        assert list(s._enumerate_scalar()) == want
+        assert list(s._filter_scalar()) == want
 
 
 def test_golden_random_spaces(golden):
