@@ -20,8 +20,11 @@ plus on-device verification against the naive reference kernel.
   best configuration's output grid back.
 * ``roofline`` -- the best configuration's dominant launch against its
   binding ceiling (HBM or FP32), measured with CUDA events in the run.
-* ``cpu_baseline`` -- the oracle port of the reference loop (CPU kernel,
-  all host threads) on a bounded sample, rank 0 only.
+* ``cpu_baseline`` -- the reference's own CPU path on a bounded sample,
+  rank 0 only: the UNMODIFIED reference (baseline/_ref) running its random
+  search with its command backend over ``oracle/tsbench_cpu`` (the C
+  kernel, all host threads); the oracle port of that loop if the reference
+  is not installed (``kind`` says which).
 
 * ``kernels`` -- the other four tuned kernels (convolution, dedispersion,
   GEMM fp32, GEMM tf32 tcgen05), measured in the same run after the
@@ -314,43 +317,71 @@ def step_configs(space, wl, batch, seed, step, rank, world):
     return stratified_sample(space, batch, seed, wl["param"], offset=offset)
 
 
-def run_cpu_baseline(workload: str, configs: list, budget_s: float, protocol_runs=(1, 7)) -> dict:
-    """Oracle port of the reference loop on the host (bounded sample)."""
+def run_cpu_baseline(workload: str, configs: list, budget_s: float, seed: int = 0) -> dict:
+    """The reference's CPU path on the host, bounded sample.
+
+    Preferred (``kind: "reference"``): the UNMODIFIED reference installed
+    under baseline/_ref runs its own random search, its command backend
+    timing the C kernel program ``oracle/tsbench_cpu`` (oracle/reference_arm.py).
+    Fallback (``kind: "port"``): the oracle port of that loop.
+    """
+    from oracle import reference_arm
+
+    if reference_arm.available() and workload in ("hotspot", "convolution", "gemm"):
+        done = secs = 0.0
+        parts = []
+        while True:  # one configuration per reference search, until the budget is spent
+            r = reference_arm.timed_random_search(workload, 1, seed + len(parts))
+            parts.append(r)
+            done += r["configs"]
+            secs += r["seconds"]
+            if secs >= budget_s:
+                break
+        return {"configs": int(done), "seconds": secs, "cores": parts[0]["cores"], "kind": "reference",
+                "sample": f"{int(done)} x ({parts[0]['sample']})"}
     from oracle import reference_port
 
-    return reference_port.timed_sample(workload, configs, budget_s=budget_s,
-                                       warmup=protocol_runs[0], runs=protocol_runs[1])
+    r = reference_port.timed_sample(workload, configs, budget_s=budget_s)
+    r["kind"] = "port"
+    return r
 
 
 def reference_arm(args, dist: Dist):
     if dist.rank != 0:
         return
+    from oracle import reference_arm as ref
     from paper_2407_11488_b200.problems import make_problem
 
     wl = WORKLOADS[args.workload]
     prob = make_problem(args.workload)
-    per_step = []
-    total_cfg = 0
-    info = None
+    use_ref = ref.available() and args.workload in ("hotspot", "convolution", "gemm")
+    per_step, total_cfg, info = [], 0, None
     steps = args.warmup + args.steps
     for s in range(steps):
-        cfgs = step_configs(prob.space, wl, 2, args.seed + 17, s, 0, 1)
-        r = run_cpu_baseline(args.workload, cfgs, budget_s=max(2.0, args.cpu_sample_s / steps))
+        if use_ref:  # the unmodified reference's random search: one configuration per step
+            r = ref.timed_random_search(args.workload, 1, args.seed + 17 + s)
+        else:
+            cfgs = step_configs(prob.space, wl, 2, args.seed + 17, s, 0, 1)
+            r = run_cpu_baseline(args.workload, cfgs, budget_s=max(2.0, args.cpu_sample_s / steps))
         info = r
         if s >= args.warmup:
             per_step.append(r["seconds"])
             total_cfg += r["configs"]
     secs = sum(per_step)
     value = total_cfg / secs if secs > 0 else 0.0
+    kind = "reference" if use_ref else info.get("kind", "port")
+    executor = ("UNMODIFIED reference (tunescape 0.1.0 from baseline/_ref): random_search + command backend "
+                "running oracle/tsbench_cpu (C kernel, all host threads)" if use_ref else
+                "oracle port of the reference loop (C kernel, all host threads)")
     line = {
         "impl": "reference", "metric": metric_name(), "value": round(value, 4), "unit": "configs/s",
         "n_gpus": args.gpus, "ranks": dist.world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1000 * secs / max(1, args.steps), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": wl["desc"], "configs_per_step": 2, "protocol": "1 warmup + 7 runs, mean",
-                   "executor": "oracle port of the reference loop (C kernel, all host threads)"},
+        "config": {"workload": wl["desc"], "configs_per_step": 1 if use_ref else 2,
+                   "protocol": "1 warmup + 7 runs, mean", "executor": executor},
         "cpu_baseline": {"value": round(value, 4), "unit": "configs/s", "cores": info["cores"],
-                         "kind": "port", "sample": info["sample"]},
+                         "kind": kind, "sample": info["sample"]},
         "e2e": {"value": round(value, 4), "unit": "configs/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -667,9 +698,9 @@ def our_arm(args, dist: Dist):
     cpu = None
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         try:
-            r = run_cpu_baseline(args.workload, timed_sets[0][:4], budget_s=args.cpu_sample_s)
+            r = run_cpu_baseline(args.workload, timed_sets[0][:4], budget_s=args.cpu_sample_s, seed=args.seed)
             cpu = {"value": round(r["configs"] / r["seconds"], 4), "unit": "configs/s",
-                   "cores": r["cores"], "kind": "port", "sample": r["sample"]}
+                   "cores": r["cores"], "kind": r["kind"], "sample": r["sample"]}
         except Exception as e:  # noqa: BLE001 -- baseline is reported, never fatal
             cpu = {"value": None, "unit": "configs/s", "cores": None, "kind": "port",
                    "sample": f"unavailable: {e}"}

@@ -11,7 +11,10 @@ reference's ``command_execute`` (`pkg/src/tunescape/measure.py:218-305`):
 3. warmup + benchmark runs in ONE native call, per-run CUDA events on
    the launch stream, optional L2 flush outside the events; a rejected
    launch -> ``invalid``, a device fault -> ``runtime_failed`` (the
-   context is poisoned; the multi-GPU runner respawns the worker), the
+   context is poisoned: every later configuration raises
+   :class:`DevicePoisoned` instead of recording a fake failure, so the sweep
+   stops, nothing unmeasured reaches the cache or the resume log, and a
+   restarted process -- a fresh context -- measures the rest), the
    watchdog -> ``timeout``;
 4. on-device verification against the answer buffer (no D2H of the
    output), mismatch -> ``runtime_failed`` with the error in ``detail``.
@@ -39,6 +42,16 @@ from .paramspace import config_key
 _RC_STATUS = {rt.ERR_COMPILE: Status.COMPILE_FAILED, rt.ERR_INVALID: Status.INVALID,
               rt.ERR_RUNTIME: Status.RUNTIME_FAILED, rt.ERR_TIMEOUT: Status.TIMEOUT,
               rt.ERR_ARG: Status.INVALID}
+
+
+class DevicePoisoned(DeviceError):
+    """A device fault poisoned this process's CUDA context: no further
+    configuration can be measured in it (restart the worker; ``--resume``
+    re-measures everything not yet logged)."""
+
+    def __init__(self, index: int):
+        super().__init__(f"CUDA context of device {index} poisoned by an earlier fault; "
+                         "restart the worker (with --resume) to measure the remaining configurations")
 
 
 def default_workers() -> int:
@@ -235,8 +248,7 @@ class CudaTarget:
     # -- the protocol ------------------------------------------------------------------
     def execute(self, config, protocol: MeasurementProtocol) -> Observation:
         if self.dev.poisoned:
-            return Observation(Status.RUNTIME_FAILED,
-                               detail="device context poisoned by an earlier fault")
+            raise DevicePoisoned(self.dev.index)
         names = self.problem.space.param_names
         cfg = dict(zip(names, config))
         key = config_key(config)
@@ -451,7 +463,7 @@ class CudaTarget:
             info["t_abs_prepare"] = t0
             immediate = None
             if self.dev.poisoned:
-                immediate = Observation(Status.RUNTIME_FAILED, detail="device context poisoned by an earlier fault")
+                raise DevicePoisoned(self.dev.index)
             else:
                 prep = self._prepare(config, info)
                 if isinstance(prep, Observation):

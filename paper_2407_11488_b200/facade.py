@@ -300,7 +300,9 @@ class GenericTarget:
 
     def execute(self, config, protocol: MeasurementProtocol) -> Observation:
         if self.dev.poisoned:
-            return Observation(Status.RUNTIME_FAILED, detail="device context poisoned")
+            from .cuda_backend import DevicePoisoned
+
+            raise DevicePoisoned(self.dev.index)
         inst, res = self._get(config)
         if not res.ok:
             return Observation(Status.COMPILE_FAILED, detail=(res.error or res.log)[-2000:])
