@@ -568,14 +568,25 @@ def our_arm(args, dist: Dist):
     sampler = ClockSampler(dist.local)
     sampler.start()
 
-    # -- warmup steps double as the COLD measurement (NVRTC pipelined) -------
-    cold_cfg, cold_s = 0, 0.0
-    for s in range(args.warmup):
-        cfgs = step_configs(space, wl, batch, args.seed, s, dist.rank, dist.world)
-        t0 = time.perf_counter()
-        run_step(cfgs)
-        cold_s += time.perf_counter() - t0
-        cold_cfg += len(cfgs)
+    # -- one-time process setup (untimed, reported as setup_s): the on-device
+    # answer (naive reference chain), NVRTC/driver first-use initialisation,
+    # one priming configuration from outside every measured set
+    t_prime = time.perf_counter()
+    target.answer()
+    prime = step_configs(space, wl, 1, args.seed + 991, args.warmup + args.steps + 1, dist.rank, dist.world)
+    run_step(prime)
+    setup_s += time.perf_counter() - t_prime
+
+    # -- warmup steps double as the COLD measurement: NVRTC compilation
+    # pipelined with the device (one list, like the timed region) ----------
+    cold_list = [c for s in range(args.warmup)
+                 for c in step_configs(space, wl, batch, args.seed, s, dist.rank, dist.world)]
+    compiled0 = compiler.stats["compiled"]
+    t0 = time.perf_counter()
+    run_step(cold_list)
+    cold_s = time.perf_counter() - t0
+    cold_cfg = len(cold_list)
+    cold_compiles = compiler.stats["compiled"] - compiled0
     dist.barrier()
     cold_rate = dist.sum(cold_cfg) / dist.max(cold_s) if cold_s else 0.0
 
@@ -734,6 +745,11 @@ def our_arm(args, dist: Dist):
                        "verify": "every config checked on-device vs the naive reference kernel",
                        "parallelism": f"config shards x{dist.world} (no data-path collective)"},
             "cold": {"value": round(cold_rate, 3), "unit": "configs/s",
+                     "configs": cold_cfg, "seconds": round(cold_s, 3),
+                     "nvrtc_compilations": cold_compiles,
+                     "note": "warm-up steps as one pipelined list, NVRTC inside the loop (fresh cubin "
+                             "cache); stream-mode configurations differing only in launch geometry "
+                             "share a cubin",
                      "compile_workers": compiler.pool._max_workers,
                      "precompile_s": round(precompile_s, 3)},
             "best_config": best, "best_config_per_rank": all_best if dist.world > 1 else None,

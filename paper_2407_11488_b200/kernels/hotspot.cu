@@ -112,7 +112,12 @@ struct HsCoef {
 #define TA (((TT) + 3) & ~3)
 #define UW (((SW - TA - TT) / 4) * 4)
 #define NSTRIPS ((GW + UW - 1) / UW)
-#define NTHREADS (BSX * BSY)
+// Stream kernels are compiled per THREAD COUNT, not per (BSX, BSY): the
+// unit of work is a warp, so block shape and TSY (waves, a launch-geometry
+// choice) never reach the code -- configurations that differ only there
+// share one cubin (problems.Hotspot.config_defines; 105,412 configurations
+// -> 5,762 compilations).
+#define NTHREADS (HS_THREADS)
 #define WPB (NTHREADS / 32)
 // input ring: NR rows = NG groups of 2 rows (one group per iteration),
 // NG-1 groups in flight
@@ -588,7 +593,7 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
                                                float ax, float ap, float ac, int segh, int nsegs,
                                                int segh0) {
   extern __shared__ __align__(128) float smem[];
-  const int tid = threadIdx.y * BSX + threadIdx.x;
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int wid = tid >> 5;
   const int g = (int)blockIdx.x * WPB + wid;
   if (g >= NSTRIPS * nsegs) return;  // whole warp; no block barrier follows
