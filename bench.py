@@ -71,7 +71,7 @@ WORKLOADS = {
     "dedispersion": dict(param="block_size_x", batch=8,
                          desc="dedispersion 1536 ch x 2048 DM x 25000 samples fp32"),
     "gemm": dict(param="VWM", batch=12, desc="gemm 4096^3 fp32 CLBlast space"),
-    "gemm_tc": dict(param=None, batch=8, desc="gemm 4096^3 tf32 tcgen05/TMEM/TMA variant (BN_T x STAGES)"),
+    "gemm_tc": dict(param=None, batch=8, desc="gemm 4096^3 tf32 tcgen05/TMEM/TMA variant (BN_T x STAGES x CLUSTER)"),
     "dd_hotspot": dict(param=None, batch=1, desc="domain-decomposed hotspot 16384x16384 fp32, 20 iterations, "
                                                  "one row slab per rank, NCCL halo exchange"),
 }
@@ -81,7 +81,7 @@ KERNEL_SAMPLES = {
     "convolution": ([(256, 2, 4, 4, 1, 0, 0)], "tile_size_y", 11),
     "dedispersion": ([(32, 32, 4, 8, 1, 0)], "block_size_x", 7),
     "gemm": ([(128, 64, 16, 16, 8, 16, 8, 4, 4, 1, 1, 1, 1)], "VWM", 9),
-    "gemm_tc": ([(256, 2)], None, 7),
+    "gemm_tc": ([(256, 2, 1), (256, 2, 2)], None, 6),
 }
 
 

@@ -17,7 +17,17 @@
 //               tcgen05.commit frees the smem stage / signals the epilogue
 //   warps 2-5   epilogue: tcgen05.ld 32x32b (TMEM lane = m) -> registers
 //               -> coalesced column stores of C (m contiguous)
-// Tunables (compile-time): BN_T, STAGES.  Problem macros: GM, GN, GK.
+// CLUSTER == 2: a 2-CTA thread-block cluster shares the B tile -- the two
+// CTAs own consecutive M tiles of the same N tile; each TMA-loads its own
+// A box and HALF of the B box, multicast into both CTAs' stage buffers
+// (cp.async.bulk.tensor ... .multicast::cluster), so L2->SM operand traffic
+// per output drops from (128+BN_T) to (128+BN_T/2) rows per k-block (the
+// single-CTA kernel is bound by it: ~18 TB/s of TMA reads, ncu
+// profiles/round2/ncu/ncu_gemm_tc_256-2.md).  A stage may be refilled only
+// when BOTH CTAs' MMAs have consumed it: every MMA commit arrives on the
+// empty barrier of both CTAs (tcgen05.commit ... .multicast::cluster), whose
+// count is 2.
+// Tunables (compile-time): BN_T, STAGES, CLUSTER.  Problem macros: GM, GN, GK.
 // Precision: operands are read as TF32 (10-bit mantissa) by the tensor
 // core, accumulation is fp32; verification uses a K-scaled tolerance.
 
@@ -26,6 +36,9 @@
 #endif
 #ifndef STAGES
 #define STAGES 4
+#endif
+#ifndef CLUSTER
+#define CLUSTER 1
 #endif
 #define BM 128
 #define BK 32
@@ -109,6 +122,33 @@ __device__ __forceinline__ void umma_commit(unsigned bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
+// commit arriving on the barrier at the same smem offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mc(unsigned bar, unsigned short mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+               "h"(mask)
+               : "memory");
+}
+
+// TMA 2-D load multicast into the same smem offset of every CTA in `mask`;
+// each destination CTA's mbarrier (same offset) receives the byte count
+__device__ __forceinline__ void tma_load_2d_mc(unsigned dst, const TmaDesc* desc, int c0, int c1, unsigned bar,
+                                               unsigned short mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(desc)), "r"(c0), "r"(c1), "r"(bar), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
                const __grid_constant__ TmaDesc tma_b, int tiles_m, int n_full) {
@@ -132,19 +172,30 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   // as the others (512 whole tiles on 148 SMs would cap at 86.5%).  A half
   // tile still TMA-loads a full BN_T-row B box (rows past its own 128 are
   // unused / zero-filled past GN) and runs the MMA with N = BN_T/2.
+#if CLUSTER == 2
+  // a cluster owns M tiles (2p, 2p+1) of one N tile; whole tiles only
+  const unsigned crank = cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  const int pairs_m = tiles_m >> 1;
+  const int m0 = ((pair % pairs_m) * 2 + (int)crank) * BM;
+  const int bn = BN_T;
+  const int n0 = (pair / pairs_m) * BN_T;
+  (void)n_full;
+#else
   const int item = blockIdx.x;
   const int tile = item < n_full ? item : n_full + ((item - n_full) >> 1);
   const int half = item < n_full ? -1 : ((item - n_full) & 1);
   const int m0 = (tile % tiles_m) * BM;
   const int bn = half < 0 ? BN_T : BN_T / 2;
   const int n0 = (tile / tiles_m) * BN_T + (half > 0 ? BN_T / 2 : 0);
+#endif
   const unsigned idesc = IDESC_N(bn);
   constexpr int KB = GK / BK;
 
   if (warp == 0 && lane == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full0 + 8 * s, 1);
-      mbar_init(empty0 + 8 * s, 1);
+      mbar_init(empty0 + 8 * s, CLUSTER);  // every CTA of the cluster releases the stage
     }
     mbar_init(tfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -158,6 +209,9 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+#if CLUSTER == 2
+  cluster_sync_all();  // the peer's barriers are initialised before anything targets them
+#endif
   asm volatile("tcgen05.fence::after_thread_sync;");
   const unsigned tmem = *tmem_slot;
 
@@ -172,7 +226,13 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
         const unsigned sa = sbase + s * STAGE_BYTES;
         const unsigned sb = sa + A_STAGE_BYTES;
         tma_load_2d(sa, &tma_a, kb * BK, m0, full);  // coords: (k, m)
+#if CLUSTER == 2
+        // this CTA's half of the B box, into both CTAs (same offset)
+        tma_load_2d_mc(sb + crank * (B_STAGE_BYTES / 2), &tma_b, kb * BK, n0 + (int)crank * (BN_T / 2), full,
+                       (unsigned short)0x3);
+#else
         tma_load_2d(sb, &tma_b, kb * BK, n0, full);  // coords: (k, n)
+#endif
       }
     }
   } else if (warp == 1) {
@@ -202,7 +262,11 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
           (void)db;
 #endif
         }
+#if CLUSTER == 2
+        umma_commit_mc(empty0 + 8 * s, (unsigned short)0x3);  // releases the stage in both CTAs
+#else
         umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs retire
+#endif
       }
       umma_commit(tfull);  // accumulator complete
     }
@@ -247,6 +311,9 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
+#if CLUSTER == 2
+  cluster_sync_all();  // no peer multicast or commit may still target this CTA's smem
+#endif
   if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));

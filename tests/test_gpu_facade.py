@@ -95,3 +95,75 @@ def test_tsbench_through_command_backend():
     be = command_backend(tpl)
     obs = measure(be, (32, 8, 2, 2, 5, 5, 1), MeasurementProtocol(), space.param_names)
     assert obs.ok and len(obs.times_ms) == 7, obs
+
+
+def test_unmodified_reference_tune_drives_b200_kernels(tmp_path):
+    """The UNMODIFIED reference (tunescape installed under baseline/_ref by
+    baseline/install_reference.sh) runs its own ``tune`` command line with a
+    ``cmd:`` backend over tsbench: its random search, process protocol and
+    stdout parsing measure B200 kernels, and its cache holds them."""
+    import json
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    ref = root / "baseline" / "_ref"
+    if not (ref / "tunescape" / "__init__.py").exists():
+        pytest.skip("reference not installed (baseline/install_reference.sh)")
+    tpl = (f"{sys.executable} -m paper_2407_11488_b200.tsbench --kernel hotspot --size width=1024,height=1024 "
+           "--config {block_size_x},{block_size_y},{tile_size_x},{tile_size_y},"
+           "{temporal_tiling_factor},{loop_unroll_factor_t},{sh_power}")
+    out = tmp_path / "b200_via_reference.json"
+    env = dict(os.environ, PYTHONPATH=os.pathsep.join([str(ref), str(root)]))
+    proc = subprocess.run([sys.executable, "-c", "import sys, tunescape.cli as c; "
+                           "assert 'baseline/_ref' in c.__file__, c.__file__; sys.argv[0] = 'tunescape'; c.main()",
+                           "tune", "--space", "hotspot", "--backend", f"cmd:{tpl}", "--strategy", "random",
+                           "--budget", "3", "--seed", "5", "--out", str(out)],
+                          capture_output=True, text=True, env=env, timeout=900, cwd=str(root))
+    assert proc.returncode == 0, proc.stderr[-3000:]
+    assert "evaluations : 3" in proc.stdout and "best config : " in proc.stdout, proc.stdout
+    doc = json.loads(out.read_text())
+    oks = [r for r in doc["records"].values() if r["status"] == "ok"]
+    assert len(doc["records"]) == 3 and oks and all(len(r["times_ms"]) == 7 for r in oks)
+
+
+TRAP_KERNEL = r"""
+extern "C" __global__ void maybe_trap(float* c, const float* a, int n) {
+  int i = blockIdx.x * block_size_x + threadIdx.x;
+  if (block_size_x == 64) __trap();  // a device fault in exactly one configuration
+  if (i < n) c[i] = a[i] * 2.0f;
+}
+"""
+
+TRAP_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from paper_2407_11488_b200 import tune_kernel
+from paper_2407_11488_b200.cuda_backend import DevicePoisoned
+n = 4096
+a = np.ones(n, np.float32)
+c = np.zeros_like(a)
+try:
+    tune_kernel("maybe_trap", sys.argv[2], n, [c, a, np.int32(n)], {"block_size_x": [32, 64, 128, 256]})
+    print("NO-RAISE")
+except DevicePoisoned as e:
+    print("POISONED", e)
+"""
+
+
+def test_device_fault_stops_the_sweep(tmp_path):
+    """A configuration that faults the device poisons the process's CUDA
+    context; the sweep must stop with DevicePoisoned instead of recording
+    fake failures for the configurations after it (they are re-measured by a
+    restarted, resumed run).  Isolated in a subprocess: the context is dead
+    afterwards."""
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    proc = subprocess.run([sys.executable, "-c", TRAP_SCRIPT, str(root), TRAP_KERNEL], capture_output=True,
+                          text=True, timeout=600)
+    assert "POISONED" in proc.stdout, (proc.stdout[-2000:], proc.stderr[-2000:])

@@ -212,9 +212,10 @@ def test_gemm_tc_tf32_within_k_scaled_tolerance(device):
     big = GemmTC()
     tgt = CudaTarget(big, device=device)
     try:
-        obs = tgt.execute((256, 4), PROTO)
-        assert obs.ok, obs
-        assert tgt.extras["256,4"]["verify"]["max_abs_err"] <= big.abs_tol
+        for c in [(256, 4, 1), (256, 2, 2)]:  # single CTA; 2-CTA cluster with multicast B
+            obs = tgt.execute(c, PROTO)
+            assert obs.ok, (c, obs)
+            assert tgt.extras[",".join(map(str, c))]["verify"]["max_abs_err"] <= big.abs_tol
     finally:
         tgt.close()
 
