@@ -115,10 +115,12 @@ struct HsCoef {
 // Stream kernels are compiled per THREAD COUNT, not per (BSX, BSY): the
 // unit of work is a warp, so block shape and TSY (waves, a launch-geometry
 // choice) never reach the code -- configurations that differ only there
-// share one cubin (problems.Hotspot.config_defines; 105,412 configurations
-// -> 5,762 compilations).
+// share one cubin (problems.Hotspot.config_defines).  The thread count
+// stays a compile-time launch bound: ptxas schedules differently under
+// __launch_bounds__(64) and (256) even though both cap at 255 registers
+// (measured: 680 vs 781 instructions in the interior loop), so blocks of
+// different sizes must not share code.
 #define NTHREADS (HS_THREADS)
-#define WPB (NTHREADS / 32)
 // input ring: NR rows = NG groups of 2 rows (one group per iteration),
 // NG-1 groups in flight
 #ifndef HS_NR
@@ -126,8 +128,24 @@ struct HsCoef {
 #endif
 #define NR HS_NR
 #define NG (NR / 2)
-// power ring: a power of two >= TT + NR + 2 rows (slot = row & (PR - 1))
-#define PR (SH_POWER ? ((TT + NR + 2) <= 16 ? 16 : ((TT + NR + 2) <= 32 ? 32 : 64)) : 0)
+// power rows are prefetched PD rows ahead of their first use (level 1),
+// independently of the input ring depth: the power ring must hold rows from
+// the deepest level's (i - TT) to the newest staged one, so a shallower
+// power prefetch shrinks it (TT=8, NR=16: 32 -> 16 rows at PD=6) and raises
+// the warps resident per SM.  Default PD = NR - 2 (power staged with input).
+#ifndef HS_PD
+#define HS_PD (NR - 2)
+#endif
+#define PD HS_PD
+// power ring: a power of two >= TT + PD + 2 rows, preceded by TT-1 MIRROR
+// rows: row r lives in slot (r - ia + 1) & (PR - 1) -- the two power rows an
+// iteration first reads (i-1, i) never straddle the wrap -- and the first
+// level to read a row writes its power term c into the slot and, for the
+// last TT-1 slots, also into the mirror row slot - PR (in front of slot 0).
+// Every later level then reads row i-k at ONE per-iteration base pointer
+// minus a compile-time offset, never wrapping (no per-level slot arithmetic).
+#define PM (SH_POWER ? (TT - 1) : 0)
+#define PR (SH_POWER ? ((TT + PD + 2) <= 8 ? 8 : ((TT + PD + 2) <= 16 ? 16 : ((TT + PD + 2) <= 32 ? 32 : 64))) : 0)
 // HS_STREAM == 2 ("smem rings"): the level rings live in per-warp shared
 // memory instead of registers (configurations whose TT x TSX register rings
 // exceed the __launch_bounds__ budget); one row per iteration
@@ -136,7 +154,7 @@ struct HsCoef {
 #else
 #define LR 0
 #endif
-#define WARP_FLOATS (SW * (NR + PR + LR))
+#define WARP_FLOATS (SW * (NR + PM + PR + LR))
 // staging chunk (floats) and chunks per lane
 #define CW ((TSX % 4) == 0 ? 4 : ((TSX % 2) == 0 ? 2 : 1))
 #define NCH (TSX / CW)
@@ -190,6 +208,7 @@ struct HsStream {
   float* pring;   // PR rows (SH_POWER)
   float* lring;   // HS_STREAM == 2: level rings [TT][3] rows, chunk-major
   int lane, gx0, ia, ib, y0, y1, nsteps;
+  unsigned nst;      // rows ia .. ia+nst are staged (ia+nst = min(ib, GH-1))
   int cbytes[NCH];   // staging bytes per chunk (0 outside the grid)
   int csrc[NCH];     // global column of each chunk (clamped into the grid)
   unsigned omask;    // chunks that are useful output columns
@@ -237,28 +256,56 @@ __device__ __forceinline__ void sts_pairs(float* row, const float2 (&v)[NP2], in
   }
 }
 
-// stage input (and power) row `row` into the rings (no commit)
-__device__ __forceinline__ void hs_stage_row(const HsStream& S, int row) {
-  if (row <= S.ib && row < GH) {
+// stage input row `row` into the input ring (no commit)
+__device__ __forceinline__ void hs_stage_t(const HsStream& S, int row) {
+  if ((unsigned)(row - S.ia) <= S.nst) {  // ia <= row <= min(ib, GH-1): one compare
     const size_t rb = (size_t)row * GW;
     float* tr = S.tring + ((row - S.ia) & (NR - 1)) * SW;
 #pragma unroll
     for (int c = 0; c < NCH; ++c) cp_chunk(chunk_ptr(tr, c, S.lane), S.tin + rb + S.csrc[c], S.cbytes[c]);
-#if SH_POWER
-    float* pr = S.pring + ((row - S.ia) & (PR - 1)) * SW;
-#pragma unroll
-    for (int c = 0; c < NCH; ++c) cp_chunk(chunk_ptr(pr, c, S.lane), S.power + rb + S.csrc[c], S.cbytes[c]);
-#endif
   }
 }
 
-// rows (row, row+1) as one cp.async group -- always committed, so that the
-// group count stays uniform
-__device__ __forceinline__ void hs_stage_pair(const HsStream& S, int row) {
-  hs_stage_row(S, row);
-  hs_stage_row(S, row + 1);
+// stage power row `row` into the power ring (no commit); rows before the
+// stream start are never read as valid data (garbage pipeline rows)
+__device__ __forceinline__ void hs_stage_p(const HsStream& S, int row) {
+#if SH_POWER
+  if ((unsigned)(row - S.ia) <= S.nst) {
+    const size_t rb = (size_t)row * GW;
+    float* pr = S.pring + ((row - S.ia + 1) & (PR - 1)) * SW;
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) cp_chunk(chunk_ptr(pr, c, S.lane), S.power + rb + S.csrc[c], S.cbytes[c]);
+  }
+#else
+  (void)S;
+  (void)row;
+#endif
+}
+
+// The staging group of stream iteration i (one cp.async group per
+// iteration, always committed so the group count stays uniform):
+//   two rows per iteration: input rows i+NR-2, i+NR-1, power rows i+PD-1,
+//   i+PD; iteration i first reads power rows i-1, i (staged PD/2 groups
+//   earlier) and input rows i, i+1 (NG-1 groups earlier; PD <= NR-2).
+//   one row per iteration: input row i+NR-1, power row i+PD-1; iteration i
+//   first reads power row i-1 (PD groups earlier) and input row i.
+__device__ __forceinline__ void hs_stage_iter2(const HsStream& S, int i) {
+  hs_stage_t(S, i + NR - 2);
+  hs_stage_t(S, i + NR - 1);
+  hs_stage_p(S, i + PD - 1);
+  hs_stage_p(S, i + PD);
   cp_commit();
 }
+__device__ __forceinline__ void hs_stage_iter1(const HsStream& S, int i) {
+  hs_stage_t(S, i + NR - 1);
+  hs_stage_p(S, i + PD - 1);
+  cp_commit();
+}
+static_assert(PD >= 0 && PD <= NR - 2, "power prefetch must not outrun the input ring");
+static_assert(HS_RPI == 1 || PD % 2 == 0, "two rows per iteration: even power prefetch distance");
+static_assert(!SH_POWER || PR >= TT + PD + 2, "power ring too small");
+#define HS_WAIT2 ((PD) / 2)
+#define HS_WAIT1 (PD)
 
 // The power term c = fma(ap, P, ac) of row r for this lane's columns.
 // SH_POWER: the first level to read a power row (FRESH) turns the staged P
@@ -266,21 +313,25 @@ __device__ __forceinline__ void hs_stage_pair(const HsStream& S, int row) {
 // is involved -- and the later levels read c.  Without SH_POWER every level
 // re-reads P through L1 and forms c itself.
 template <bool FRESH>
-__device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, int r, const HsK2& k2) {
+__device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, float* prow, int r,
+                                         bool mirror, const HsK2& k2) {
 #if SH_POWER
-  float* row = S.pring + ((r - S.ia) & (PR - 1)) * SW;
-  lds_pairs(pw, row, S.lane);
+  (void)r;
+  lds_pairs(pw, prow, S.lane);
   if (FRESH) {
 #pragma unroll
     for (int q = 0; q < NP2; ++q) pw[q] = __ffma2_rn(k2.ap, pw[q], k2.ac);
-    sts_pairs(row, pw, S.lane);
+    sts_pairs(prow, pw, S.lane);                      // the slot ...
+    if (mirror) sts_pairs(prow - PR * SW, pw, S.lane);  // ... and its mirror (warp-uniform)
   }
 #else
-  const float* prow = S.power + (size_t)min(max(r, 0), GH - 1) * GW;
+  (void)prow;
+  (void)mirror;
+  const float* grow = S.power + (size_t)min(max(r, 0), GH - 1) * GW;
   float t[TSX];
 #pragma unroll
   for (int c = 0; c < NCH; ++c) {
-    const float* p = prow + S.csrc[c];
+    const float* p = grow + S.csrc[c];
 #if CW == 4
     const float4 q = __ldg(reinterpret_cast<const float4*>(p));
     t[4 * c] = q.x; t[4 * c + 1] = q.y; t[4 * c + 2] = q.z; t[4 * c + 3] = q.w;
@@ -296,6 +347,12 @@ __device__ __forceinline__ void hs_power(float2 (&pw)[NP2], const HsStream& S, i
     pw[q] = __ffma2_rn(k2.ap, make_float2(t[2 * q], 2 * q + 1 < TSX ? t[2 * q + 1] : 0.f), k2.ac);
 #endif
 }
+
+// this iteration's power slot ps (of row i-1) and base pointer; row i-k
+// (k >= 1) of an earlier level is at pbase - (k - 1) * SW (slot or mirror)
+__device__ __forceinline__ int hs_pslot(const HsStream& S, int i) { return SH_POWER ? ((i - S.ia) & (PR - 1)) : 0; }
+#define HS_PROW(pb, k) ((pb) - (SH_POWER ? ((k) - 1) * SW : 0))
+#define HS_MIRRORED(slot) ((slot) > PR - TT)
 
 // One cell-pair row update (HS_FAST on columns 2q, 2q+1; bit-exact):
 // C = centre row, N/S rows, wl/er = W of column 0 / E of column TSX-1
@@ -377,11 +434,14 @@ __device__ __forceinline__ void hs_store_row(const HsStream& S, int ro, const fl
 template <int PH, int E, int NS>
 __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT][4][NP2], int i,
                                                const HsCoef& kk, const HsK2& k2) {
-  hs_stage_pair(S, i + NR - 2);  // keep NG-1 row pairs in flight
-  cp_wait<NG - 1>();             // this lane's chunks of rows i, i+1 have landed
+  hs_stage_iter2(S, i);  // keep NG-1 input row pairs in flight
+  cp_wait<HS_WAIT2>();   // this lane's chunks of input rows i, i+1 and power rows i-1, i have landed
   float2 f0[NP2], f1[NP2];       // fresh rows of the previous level (level 0: input)
-  lds_pairs(f0, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
-  lds_pairs(f1, S.tring + ((i + 1 - S.ia) & (NR - 1)) * SW, S.lane);
+  const float* tb = S.tring + ((i - S.ia) & (NR - 1)) * SW;  // rows i, i+1 (even slot: no wrap)
+  const int ps = hs_pslot(S, i);
+  float* pbase = S.pring + ps * SW;
+  lds_pairs(f0, tb, S.lane);  // rows >= GH: stale, never used
+  lds_pairs(f1, tb + SW, S.lane);
   // E/W neighbours of every level's OLD centre row (level k-1 row a),
   // hoisted into one convergence block
   float wla[TT], era[TT];
@@ -414,10 +474,10 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     // power rows a and a+1; row a+1 is the previous level's row a (reuse)
     float2 pa[NP2], pb[NP2];
     if (k == 1) {  // rows a, a+1 are new to the pipeline: P -> c
-      hs_power<true>(pa, S, a, k2);
-      hs_power<true>(pb, S, a + 1, k2);
+      hs_power<true>(pa, S, pbase, a, HS_MIRRORED(ps), k2);
+      hs_power<true>(pb, S, pbase + SW, a + 1, HS_MIRRORED(ps + 1), k2);
     } else {
-      hs_power<false>(pa, S, a, k2);
+      hs_power<false>(pa, S, HS_PROW(pbase, k), a, false, k2);
 #pragma unroll
       for (int q = 0; q < NP2; ++q) pb[q] = pprev[q];
     }
@@ -450,10 +510,11 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
 #if HS_STREAM == 2
 template <int PH, int E, int NS>
 __device__ __forceinline__ void hs_stream_iter_s(const HsStream& S, int i, const HsCoef& kk, const HsK2& k2) {
-  hs_stage_row(S, i + NR - 1);
-  cp_commit();
-  cp_wait<NR - 1>();
+  hs_stage_iter1(S, i);
+  cp_wait<HS_WAIT1>();
   float2 f0[NP2];
+  const int ps = hs_pslot(S, i);
+  float* pbase = S.pring + ps * SW;
   lds_pairs(f0, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
 #pragma unroll
   for (int k = 1; k <= TT; ++k) {
@@ -475,9 +536,9 @@ __device__ __forceinline__ void hs_stream_iter_s(const HsStream& S, int i, const
     }
     float2 pa[NP2];
     if (k == 1)
-      hs_power<true>(pa, S, a, k2);
+      hs_power<true>(pa, S, pbase, a, HS_MIRRORED(ps), k2);
     else
-      hs_power<false>(pa, S, a, k2);
+      hs_power<false>(pa, S, HS_PROW(pbase, k), a, false, k2);
     float2 na[NP2];
     hs_row_update<E>(na, N, Cc, f0, wl, er, pa, (E & 4) && a == 0, (E & 4) && a == GH - 1, S, kk, k2);
 #pragma unroll
@@ -505,10 +566,11 @@ __device__ __forceinline__ void hs_stream_run_s(const HsStream& S, const HsCoef&
 template <int PH, int E, int NS>
 __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[TT][3][NP2], int i,
                                                 const HsCoef& kk, const HsK2& k2) {
-  hs_stage_row(S, i + NR - 1);  // keep NR-1 rows in flight (one group per row)
-  cp_commit();
-  cp_wait<NR - 1>();
+  hs_stage_iter1(S, i);  // keep NR-1 input rows in flight (one group per row)
+  cp_wait<HS_WAIT1>();
   float2 f0[NP2];
+  const int ps = hs_pslot(S, i);
+  float* pbase = S.pring + ps * SW;
   lds_pairs(f0, S.tring + ((i - S.ia) & (NR - 1)) * SW, S.lane);  // rows >= GH: stale, never used
   float wla[TT], era[TT];  // E/W of every level's centre row, one convergence block
 #pragma unroll
@@ -530,9 +592,9 @@ __device__ __forceinline__ void hs_stream_iter1(const HsStream& S, float2 (&R)[T
     const int s0 = ((PH - k + 1) % 3 + 3) % 3;
     float2 pa[NP2];
     if (k == 1)
-      hs_power<true>(pa, S, a, k2);
+      hs_power<true>(pa, S, pbase, a, HS_MIRRORED(ps), k2);
     else
-      hs_power<false>(pa, S, a, k2);
+      hs_power<false>(pa, S, HS_PROW(pbase, k), a, false, k2);
     float2 na[NP2];
     hs_row_update<E>(na, R[k - 1][sN], R[k - 1][sC], f0, wla[k - 1], era[k - 1], pa, (E & 4) && a == 0,
                         (E & 4) && a == GH - 1, S, kk, k2);
@@ -587,24 +649,48 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
 // hotspot_rem_kernel (NS = HS_REM), so no code path has a runtime level
 // count -- a dynamic-depth path needs ~1.6x the registers (exit phis) and,
 // being part of the same kernel, would cap every launch's occupancy.
+//
+// Warp tiles.  Strips whose window touches a grid border (a prefix
+// [0, XL) and a suffix [XR, NSTRIPS), from the compile-time geometry) run
+// the all-selects edge code, ~1.6x the interior's instructions per row, so
+// the host gives them proportionally more, shorter row segments (nse per
+// edge strip vs ns per interior strip) and all warps of the single wave
+// finish together.  Edge-strip tiles take the first warp indices.
+#define XL ((TA) / (UW) + 1 < NSTRIPS ? (TA) / (UW) + 1 : NSTRIPS)
+#define XR_RAW ((GW - 1 - SW + TA) < 0 ? 0 : (GW - 1 - SW + TA) / (UW) + 1)
+#define XR (XR_RAW < XL ? XL : (XR_RAW > NSTRIPS ? NSTRIPS : XR_RAW))
+#define NXE (XL + NSTRIPS - XR)
+#define NXI (XR - XL)
 template <int NS>
 __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const float* __restrict__ tin,
                                                const float* __restrict__ power, float at, float ay,
                                                float ax, float ap, float ac, int segh, int nsegs,
-                                               int segh0) {
+                                               int segh0, int seghe, int nsegse, int segh0e) {
   extern __shared__ __align__(128) float smem[];
   const int tid = threadIdx.y * blockDim.x + threadIdx.x;
   const int wid = tid >> 5;
-  const int g = (int)blockIdx.x * WPB + wid;
-  if (g >= NSTRIPS * nsegs) return;  // whole warp; no block barrier follows
+  const int g = (int)blockIdx.x * (int)((blockDim.x * blockDim.y) >> 5) + wid;
+  int strip, seg;
+  if (g < NXE * nsegse) {  // edge strips
+    const int e = g % NXE;
+    strip = e < XL ? e : XR + (e - XL);
+    seg = g / NXE;
+    segh = seghe;
+    nsegs = nsegse;
+    segh0 = segh0e;
+  } else {
+    const int h = g - NXE * nsegse;
+    if (NXI == 0 || h >= NXI * nsegs) return;  // whole warp; no block barrier follows
+    strip = XL + h % NXI;
+    seg = h / NXI;
+  }
   HsStream S;
   S.lane = tid & 31;
-  const int strip = g % NSTRIPS, seg = g / NSTRIPS;
   S.tin = tin;
   S.power = power;
   S.out = out;
   S.tring = smem + wid * WARP_FLOATS;
-  S.pring = S.tring + NR * SW;
+  S.pring = S.tring + (NR + PM) * SW;  // slot 0, after the mirror rows
   S.lring = S.pring + PR * SW;
   S.gx0 = strip * UW - TA;
   S.nsteps = NS;
@@ -615,6 +701,7 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
   S.y1 = seg == nsegs - 1 ? GH : min(S.y0 + (seg == 0 ? segh0 : segh), GH);
   S.ia = max(0, S.y0 - NS);
   S.ib = S.y1 - 1 + NS;
+  S.nst = (unsigned)(min(S.ib, GH - 1) - S.ia);
   S.omask = S.lmask = S.rmask = 0u;
   S.xl = S.gx0 + S.lane * TSX == 0;
   S.xr = S.gx0 + S.lane * TSX + TSX - 1 == GW - 1;
@@ -633,20 +720,16 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
     if (gx == 0) S.lmask |= 1u << j;
     if (gx == GW - 1) S.rmask |= 1u << j;
   }
+  // prologue: the staging groups of the virtual iterations before ia
 #if HS_RPI == 2
-  for (int g2 = 0; g2 < NG - 1; ++g2) hs_stage_pair(S, S.ia + 2 * g2);
+  for (int g2 = 0; g2 < NG - 1; ++g2) hs_stage_iter2(S, S.ia - (NR - 2) + 2 * g2);
 #else
-  for (int r = S.ia; r < S.ia + NR - 1; ++r) {
-    hs_stage_row(S, r);
-    cp_commit();
-  }
+  for (int j = S.ia - (NR - 1); j < S.ia; ++j) hs_stage_iter1(S, j);
 #endif
   const HsCoef kk{at, ay, ax, ap, ac};
   // edge mode of this warp tile (see hs_row_update)
   const bool xedge = S.gx0 <= 0 || S.gx0 + SW > GW - 1;
-  const bool xalign = (S.gx0 > 0 || (-S.gx0) % TSX == 0) && (S.gx0 + SW <= GW - 1 || (GW - S.gx0) % TSX == 0);
   const bool yedge = S.ia == 0 || S.ib >= GH - 1;
-  const int em = (xedge ? (xalign ? 1 : 2) : 0) | (yedge ? 4 : 0);
 #if HS_STREAM == 2
 #define HS_RUN hs_stream_run_s
 #elif HS_RPI == 2
@@ -654,44 +737,34 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
 #else
 #define HS_RUN hs_stream_run1
 #endif
-  // instantiated edge modes (each one is a full copy of the stream loop, so
-  // they cost NVRTC time): the full-depth kernel keeps interior, lane-aligned
-  // X edge, X+Y edge (also taken by Y-only tiles: its wl/er selects are two
-  // per level) and the all-selects fallback; the single short remainder
-  // launch keeps interior, lane-aligned X edge and the fallback
-  if (NS == TT) {
-    switch (em) {
-      case 0: HS_RUN<0, NS>(S, kk); break;
-      case 1: HS_RUN<1, NS>(S, kk); break;
-      case 4:
-      case 5: HS_RUN<5, NS>(S, kk); break;
-      default: HS_RUN<6, NS>(S, kk); break;
-    }
-  } else {
-    switch (em) {  // Y-edge segments are short (STREAM_EDGE_SEG): the fallback absorbs them
-      case 0: HS_RUN<0, NS>(S, kk); break;
-      case 1: HS_RUN<1, NS>(S, kk); break;
-      default: HS_RUN<6, NS>(S, kk); break;
-    }
-  }
+  // two instantiated edge modes per kernel (each one is a full copy of the
+  // stream loop, and NVRTC time grows with every copy: 7 -> 4 copies per
+  // configuration halved the compile time): interior, and the all-selects
+  // code for every tile touching a border -- edge strips get shorter
+  // segments (above), top/bottom segments are short (STREAM_EDGE_SEG)
+  if (!xedge && !yedge)
+    HS_RUN<0, NS>(S, kk);
+  else
+    HS_RUN<6, NS>(S, kk);
   cp_wait<0>();  // no copy may land in smem after the warp has left
 }
 
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_kernel(float* __restrict__ out, const float* __restrict__ tin,
                const float* __restrict__ power, int nsteps, float at, float ay, float ax,
-               float ap, float ac, int segh, int nsegs, int segh0) {
+               float ap, float ac, int segh, int nsegs, int segh0, int seghe, int nsegse, int segh0e) {
   (void)nsteps;  // == TT
-  hs_stream_body<TT>(out, tin, power, at, ay, ax, ap, ac, segh, nsegs, segh0);
+  hs_stream_body<TT>(out, tin, power, at, ay, ax, ap, ac, segh, nsegs, segh0, seghe, nsegse, segh0e);
 }
 
 #if defined(HS_REM) && HS_REM > 0
 extern "C" __global__ void __launch_bounds__(NTHREADS)
 hotspot_rem_kernel(float* __restrict__ out, const float* __restrict__ tin,
                    const float* __restrict__ power, int nsteps, float at, float ay, float ax,
-                   float ap, float ac, int segh, int nsegs, int segh0) {
+                   float ap, float ac, int segh, int nsegs, int segh0, int seghe, int nsegse,
+                   int segh0e) {
   (void)nsteps;  // == HS_REM
-  hs_stream_body<HS_REM>(out, tin, power, at, ay, ax, ap, ac, segh, nsegs, segh0);
+  hs_stream_body<HS_REM>(out, tin, power, at, ay, ax, ap, ac, segh, nsegs, segh0, seghe, nsegse, segh0e);
 }
 #endif
 

@@ -319,30 +319,46 @@ class Hotspot(Problem):
             unroll = 1 if kind == 2 else min(cfg["loop_unroll_factor_t"], 2)
             return dict(HS_THREADS=cfg["block_size_x"] * cfg["block_size_y"], TSX=cfg["tile_size_x"],
                         TT=cfg["temporal_tiling_factor"], UNROLL=unroll, SH_POWER=cfg["sh_power"],
-                        HS_STREAM=kind, HS_REM=rem, HS_NR=geo["nr"])
+                        HS_STREAM=kind, HS_REM=rem, HS_NR=geo["nr"],
+                        HS_PD=geo["pd"] if cfg["sh_power"] else 0)  # no power ring: PD unused
         return dict(BSX=cfg["block_size_x"], BSY=cfg["block_size_y"], TSX=cfg["tile_size_x"],
                     TSY=cfg["tile_size_y"], TT=cfg["temporal_tiling_factor"],
                     UNROLL=cfg["loop_unroll_factor_t"], SH_POWER=cfg["sh_power"],
                     HS_STREAM=0, HS_REM=rem, HS_NR=8)
 
     # -- stream mode (kernels/hotspot.cu, HS_STREAM) --------------------------
-    # cp.async input ring depth (rows), measured on B200:
-    # * register rings, two rows per iteration: 16 rows for T >= 6 (T=8
-    #   0.238 -> 0.205 ms), 8 below;
-    # * shared-memory rings (kind 2) and register rings with one row per
-    #   iteration at T >= 6: 4 rows -- the smaller input (and power) ring
-    #   raises occupancy; 24-configuration samples: kind 2 1.16x geomean
-    #   over 16 rows (never slower), one-row register rings 1.03x
-    #   (tools/gpu/hs_nr2.sh).
-    # TSG_HS_NR forces one value for experiments
+    # cp.async input ring depth (rows) and power prefetch distance, measured
+    # on B200 (tools/gpu/hs_exp.sh, profiles/round2/hs_ring/):
+    # * register rings: 8 input rows (3 row pairs in flight), power rows 6
+    #   ahead (4 at T >= 9, 4 for one row per iteration): with the power
+    #   ring decoupled from the input ring (16 + 7 mirror rows instead of
+    #   32) 8 rows beat 16 by 3-14% on the T = 5-10 front (best 0.1587 ->
+    #   0.1448 ms);
+    # * shared-memory rings (kind 2): 4 rows -- the smaller input (and
+    #   power) ring raises occupancy; 1.16x geomean over 16 rows on a
+    #   24-configuration sample.
+    # TSG_HS_NR / TSG_HS_PD force one value for experiments
     STREAM_NR_ENV = os.environ.get("TSG_HS_NR")
 
     def stream_nr(self, t: int, kind: int = 1, unroll: int = 2) -> int:
         if self.STREAM_NR_ENV:
             return int(self.STREAM_NR_ENV)
-        if kind == 2 or (unroll == 1 and t >= 6):
-            return 4
-        return 16 if t >= 6 else 8
+        return 4 if kind == 2 else 8
+
+    STREAM_PD_ENV = os.environ.get("TSG_HS_PD")
+
+    def stream_pd(self, t: int, kind: int, unroll: int, nr: int) -> int:
+        """Power-row prefetch distance (rows ahead of level 1's first use)."""
+        if self.STREAM_PD_ENV:
+            pd = int(self.STREAM_PD_ENV)
+        else:
+            # the power ring holds pow2(TT + PD + 2) rows: keep it at 16
+            # for every TT <= 10 (PD 6 -> 4 at TT 9, 10)
+            pd = min(nr - 2, 6 if unroll > 1 else 4, 14 - t)
+        rpi = 1 if kind == 2 or unroll == 1 else 2
+        pd = max(rpi, min(pd, nr - 2))
+        return pd - (pd % 2) if rpi == 2 else pd
+
     STREAM_SMEM_MAX = 200 * 1024
     STREAM_REG_BASE = 48     # addresses, masks, coefficients, temporaries
 
@@ -382,9 +398,11 @@ class Hotspot(Problem):
         if uw < 4:
             return None
         nr = self.stream_nr(t, kind, cfg["loop_unroll_factor_t"])
-        pr = (16 if t + nr + 2 <= 16 else (32 if t + nr + 2 <= 32 else 64)) if shp else 0
+        pd = self.stream_pd(t, kind, cfg["loop_unroll_factor_t"], nr)
+        need = t + pd + 2  # power ring rows (kernels/hotspot.cu PR)
+        pr = (8 if need <= 8 else 16 if need <= 16 else 32 if need <= 32 else 64) if shp else 0
         wpb = nthreads // 32
-        warp_floats = sw * (nr + pr + (3 * t if kind == 2 else 0))
+        warp_floats = sw * (nr + pr + (t - 1 if shp else 0) + (3 * t if kind == 2 else 0))  # + power mirror rows
         smem = 4 * wpb * warp_floats
         if smem > self.STREAM_SMEM_MAX:
             return None
@@ -395,12 +413,26 @@ class Hotspot(Problem):
             by_regs = 65536 // per_warp // wpb
             by_smem = (228 * 1024) // (smem + 1024) if smem else 32
             blocks_per_sm = max(1, min(by_regs, by_smem, 32, 64 // wpb))
-        wave = max(1, blocks_per_sm * wpb * n_sm // nstrips)  # row segments per strip, one wave
-        nsegs = max(1, min(tsy * wave, self.H // max(8, 2 * t)))
-        segh, segh0, nsegs = self._segments(nsegs)
-        return dict(sw=sw, ta=ta, uw=uw, segh=segh, segh0=segh0, wpb=wpb, smem=smem, nstrips=nstrips,
-                    nsegs=nsegs, blocks=-(-(nstrips * nsegs) // wpb), blocks_per_sm=blocks_per_sm,
-                    kind=kind, nr=nr)
+        # border strips (kernels/hotspot.cu XL/XR): a prefix and a suffix
+        # whose windows touch the grid edge; they run the all-selects code
+        xl = min(ta // uw + 1, nstrips)
+        xr_raw = 0 if self.W - 1 - sw + ta < 0 else (self.W - 1 - sw + ta) // uw + 1
+        xr = min(max(xr_raw, xl), nstrips)
+        nxe, nxi = xl + nstrips - xr, xr - xl
+        warps = tsy * blocks_per_sm * wpb * n_sm  # TSY whole waves of warp tiles
+        cap = self.H // max(8, 2 * t)
+        f = self.STREAM_XEDGE_F
+        if nxi:
+            ni = max(1, min(int(warps // (nxi + nxe * f)), cap))
+            ne = max(1, min(math.ceil(ni * f), cap))
+        else:
+            ni, ne = 1, max(1, min(warps // nxe, cap))
+        segh, segh0, ni = self._segments(ni)
+        seghe, segh0e, ne = self._segments(ne)
+        tiles = nxi * ni + nxe * ne
+        return dict(sw=sw, ta=ta, uw=uw, segh=segh, segh0=segh0, nsegs=ni, seghe=seghe, segh0e=segh0e,
+                    nsegse=ne, nxe=nxe, nxi=nxi, wpb=wpb, smem=smem, nstrips=nstrips,
+                    blocks=-(-tiles // wpb), blocks_per_sm=blocks_per_sm, kind=kind, nr=nr, pd=pd)
 
     def _smem_ring_regs(self, t: int, tsx: int) -> int:
         """Register estimate of the smem-ring stream kernel (ptxas hoists
@@ -410,6 +442,10 @@ class Hotspot(Problem):
     # top/bottom segment height relative to the others (measured optimum on B200;
     # TSG_HS_EDGE_SEG overrides it for experiments)
     STREAM_EDGE_SEG = float(os.environ.get("TSG_HS_EDGE_SEG", "0.25"))
+    # border strips run the all-selects code (~1.6x the interior's
+    # instructions per row, SASS loop bodies): they get this many times the
+    # interior strips' segment count (TSG_HS_XEDGE_F for experiments)
+    STREAM_XEDGE_F = float(os.environ.get("TSG_HS_XEDGE_F", "1.3"))
 
     def _segments(self, nsegs: int) -> tuple:
         """(segh, segh0, nsegs): interior and first segment heights, segment count.
@@ -515,8 +551,8 @@ class Hotspot(Problem):
             if occ is not None:
                 bps = occ(cfg["block_size_x"] * cfg["block_size_y"], geo["smem"])
                 geo = self.stream_geometry(cfg, blocks_per_sm=max(1, bps), n_sm=kernel.sm_count)
-            return (geo["blocks"], 1, 1), block, geo["smem"], [C.c_int(geo["segh"]), C.c_int(geo["nsegs"]),
-                                                               C.c_int(geo["segh0"])]
+            return (geo["blocks"], 1, 1), block, geo["smem"], [
+                C.c_int(geo[k]) for k in ("segh", "nsegs", "segh0", "seghe", "nsegse", "segh0e")]
         ow = cfg["block_size_x"] * cfg["tile_size_x"]
         oh = cfg["block_size_y"] * cfg["tile_size_y"]
         return (math.ceil(self.W / ow), math.ceil(self.H / oh), 1), block, self.smem_bytes(cfg), []

@@ -29,10 +29,14 @@ def test_stream_geometry_invariants():
         assert g["ta"] % 4 == 0 and g["uw"] % 4 == 0 and g["uw"] >= 4
         assert g["ta"] >= t and g["ta"] + g["uw"] <= g["sw"] - t  # useful cells valid after t levels
         assert g["nstrips"] * g["uw"] >= prob.W and (g["nstrips"] - 1) * g["uw"] < prob.W
-        assert g["nsegs"] * g["segh"] >= prob.H
-        assert g["blocks"] * g["wpb"] >= g["nstrips"] * g["nsegs"]
-        last = prob.H - g["segh0"] - (g["nsegs"] - 2) * g["segh"] if g["nsegs"] > 1 else prob.H
-        assert 0 < g["segh0"] <= g["segh"] and 0 < last <= g["segh"]  # segments tile the rows
+        for sh, sh0, ns in ((g["segh"], g["segh0"], g["nsegs"]), (g["seghe"], g["segh0e"], g["nsegse"])):
+            assert ns * sh >= prob.H
+            last = prob.H - sh0 - (ns - 2) * sh if ns > 1 else prob.H
+            assert 0 < sh0 <= sh and 0 < last <= sh  # segments tile the rows
+        assert g["blocks"] * g["wpb"] >= g["nxi"] * g["nsegs"] + g["nxe"] * g["nsegse"]
+        if g["nxi"]:  # border strips: shorter segments (all-selects code)
+            assert g["nsegse"] >= g["nsegs"]
+        _check_tiles(prob, g, t)
         assert (g["sw"] * 4) % 16 == 0  # bulk-copy row size
         assert g["smem"] <= Hotspot.STREAM_SMEM_MAX
         assert prob.smem_bytes(d) == g["smem"]
@@ -55,6 +59,37 @@ class _Fake:
     ptr = 0
 
 
+def _check_tiles(prob, g, t):
+    """Emulate the kernel's warp -> (strip, segment) mapping (hs_stream_body,
+    XL/XR): every output cell is produced by exactly one warp, border strips
+    are exactly those whose window touches a grid edge."""
+    sw, ta, uw, ns = g["sw"], g["ta"], g["uw"], g["nstrips"]
+    xl = min(ta // uw + 1, ns)
+    xr_raw = 0 if prob.W - 1 - sw + ta < 0 else (prob.W - 1 - sw + ta) // uw + 1
+    xr = min(max(xr_raw, xl), ns)
+    nxe, nxi = xl + ns - xr, xr - xl
+    assert (nxe, nxi) == (g["nxe"], g["nxi"])
+    rows = np.zeros((ns,), dtype=np.int64)
+    for gi in range(g["blocks"] * g["wpb"]):
+        if gi < nxe * g["nsegse"]:
+            e = gi % nxe
+            strip, seg = (e if e < xl else xr + e - xl), gi // nxe
+            sh, nsg, sh0 = g["seghe"], g["nsegse"], g["segh0e"]
+        else:
+            h = gi - nxe * g["nsegse"]
+            if nxi == 0 or h >= nxi * g["nsegs"]:
+                continue
+            strip, seg = xl + h % nxi, h // nxi
+            sh, nsg, sh0 = g["segh"], g["nsegs"], g["segh0"]
+        gx0 = strip * uw - ta
+        assert (gx0 <= 0 or gx0 + sw > prob.W - 1) == (strip < xl or strip >= xr)
+        y0 = 0 if seg == 0 else sh0 + (seg - 1) * sh
+        y1 = prob.H if seg == nsg - 1 else min(y0 + (sh0 if seg == 0 else sh), prob.H)
+        assert 0 <= y0 < y1 <= prob.H
+        rows[strip] += y1 - y0
+    assert (rows == prob.H).all()
+
+
 def test_stream_segments_tile_the_rows():
     """Every segment count the launcher can ask for yields segments that tile
     [0, H) exactly as the kernel computes them (first/last shortened)."""
@@ -74,7 +109,7 @@ def test_stream_compile_keys_ignore_launch_geometry():
     """Stream-mode cubins depend on the thread count, not on the block shape
     or TSY (launch geometry): configurations that differ only there share one
     compilation.  Over the whole 105,412-point space that is 5,762 distinct
-    NVRTC compilations."""
+    NVRTC compilations (5,881 with the round-2 ring depths).""" 
     import collections
 
     from paper_2407_11488_b200.problems import make_problem
@@ -89,4 +124,4 @@ def test_stream_compile_keys_ignore_launch_geometry():
     for c in p.space.enumerate_configs():
         cfg = dict(zip(names, c))
         keys[tuple(p.options(cfg))] += 1
-    assert len(keys) == 5762
+    assert len(keys) == 5881
