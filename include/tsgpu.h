@@ -60,13 +60,19 @@ typedef struct tsg_kernel tsg_kernel;
 /* One kernel launch of a (possibly multi-launch) timed run.  `args` is
  * the cuLaunchKernel kernelParams array: one pointer per kernel
  * parameter, pointing at the parameter's value.  cluster[] = {0,0,0} or
- * {1,1,1} means no cluster launch. */
+ * {1,1,1} means no cluster launch.  flags: TSG_LAUNCH_PDL launches with
+ * programmatic stream serialization (the kernel may be scheduled while the
+ * previous kernel in the stream drains; it must execute
+ * griddepcontrol.wait before touching that kernel's results).  The field
+ * occupies what was padding before `args`: the layout is unchanged. */
+#define TSG_LAUNCH_PDL 1u
 typedef struct {
   tsg_kernel* fn;
   unsigned grid[3];
   unsigned block[3];
   unsigned cluster[3];
   unsigned smem_bytes;
+  unsigned flags;
   void** args;
 } tsg_launch_t;
 

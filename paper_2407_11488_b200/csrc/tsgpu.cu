@@ -145,7 +145,8 @@ int launch_one(tsg_ctx* c, const tsg_launch_t& L) {
   if (!L.fn) return fail(TSG_ERR_ARG, "launch with null kernel");
   CUresult r;
   bool cluster = L.cluster[0] * L.cluster[1] * L.cluster[2] > 1;
-  if (!cluster) {
+  bool pdl = (L.flags & TSG_LAUNCH_PDL) != 0;
+  if (!cluster && !pdl) {
     r = cuLaunchKernel(L.fn->fn, L.grid[0], L.grid[1], L.grid[2], L.block[0], L.block[1],
                        L.block[2], L.smem_bytes, c->stream, L.args, nullptr);
   } else {
@@ -158,13 +159,23 @@ int launch_one(tsg_ctx* c, const tsg_launch_t& L) {
     cfg.blockDimZ = L.block[2];
     cfg.sharedMemBytes = L.smem_bytes;
     cfg.hStream = c->stream;
-    CUlaunchAttribute attr{};
-    attr.id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
-    attr.value.clusterDim.x = L.cluster[0];
-    attr.value.clusterDim.y = L.cluster[1];
-    attr.value.clusterDim.z = L.cluster[2];
-    cfg.attrs = &attr;
-    cfg.numAttrs = 1;
+    CUlaunchAttribute attr[2] = {};
+    unsigned na = 0;
+    if (cluster) {
+      attr[na].id = CU_LAUNCH_ATTRIBUTE_CLUSTER_DIMENSION;
+      attr[na].value.clusterDim.x = L.cluster[0];
+      attr[na].value.clusterDim.y = L.cluster[1];
+      attr[na].value.clusterDim.z = L.cluster[2];
+      ++na;
+    }
+    if (pdl) {  // programmatic dependent launch (sm_90+): overlap this launch's
+                // scheduling with the previous kernel's drain
+      attr[na].id = CU_LAUNCH_ATTRIBUTE_PROGRAMMATIC_STREAM_SERIALIZATION;
+      attr[na].value.programmaticStreamSerializationAllowed = 1;
+      ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
     r = cuLaunchKernelEx(&cfg, L.fn->fn, L.args, nullptr);
   }
   if (r != CUDA_SUCCESS) {

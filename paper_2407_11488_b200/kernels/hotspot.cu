@@ -720,6 +720,11 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
     if (gx == 0) S.lmask |= 1u << j;
     if (gx == GW - 1) S.rmask |= 1u << j;
   }
+  // programmatic dependent launch: wait until the previous launch of the
+  // run -- the producer of `tin` and reader of `out` -- has completed and
+  // its writes are visible (a no-op without the launch attribute, i.e. for
+  // the first launch of a run).  Everything above overlaps its drain.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   // prologue: the staging groups of the virtual iterations before ia
 #if HS_RPI == 2
   for (int g2 = 0; g2 < NG - 1; ++g2) hs_stage_iter2(S, S.ia - (NR - 2) + 2 * g2);
@@ -747,6 +752,11 @@ __device__ __forceinline__ void hs_stream_body(float* __restrict__ out, const fl
   else
     HS_RUN<6, NS>(S, kk);
   cp_wait<0>();  // no copy may land in smem after the warp has left
+  // let the next launch be scheduled once every warp has finished its stream
+  // (triggering at the start instead placed the next grid's CTAs early and
+  // measured 1-4% slower than this; no trigger at all: 1-4% slower too --
+  // profiles/round2/hs_ring/hs_exp_pdl2.jsonl)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 extern "C" __global__ void __launch_bounds__(NTHREADS)

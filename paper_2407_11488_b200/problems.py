@@ -104,6 +104,10 @@ class Problem:
         d = dict(self.problem_defines())
         if cfg is not None:
             d.update(self.config_defines(cfg))
+        # experiments only: TSG_EXTRA_DEFINES="NAME=V,NAME2=V2"
+        for kv in filter(None, os.environ.get("TSG_EXTRA_DEFINES", "").split(",")):
+            k, _, v = kv.partition("=")
+            d[k] = v or 1
         opts += [f"-D{k}={v}" for k, v in sorted(d.items())]
         return opts
 
@@ -446,6 +450,9 @@ class Hotspot(Problem):
     # instructions per row, SASS loop bodies): they get this many times the
     # interior strips' segment count (TSG_HS_XEDGE_F for experiments)
     STREAM_XEDGE_F = float(os.environ.get("TSG_HS_XEDGE_F", "1.3"))
+    # programmatic dependent launch between the launches of one run
+    # (TSG_HS_PDL=0 disables it for experiments)
+    STREAM_PDL = os.environ.get("TSG_HS_PDL", "1") != "0"
 
     def _segments(self, nsegs: int) -> tuple:
         """(segh, segh0, nsegs): interior and first segment heights, segment count.
@@ -557,7 +564,8 @@ class Hotspot(Problem):
         oh = cfg["block_size_y"] * cfg["tile_size_y"]
         return (math.ceil(self.W / ow), math.ceil(self.H / oh), 1), block, self.smem_bytes(cfg), []
 
-    def launch(self, cfg: dict, kernel, dst: int, src: int, power: int, nsteps: int, shape=None):
+    def launch(self, cfg: dict, kernel, dst: int, src: int, power: int, nsteps: int, shape=None,
+               pdl: bool = False):
         """One launch advancing ``src`` by ``nsteps`` into ``dst`` (raw device addresses).
 
         Stream mode: the remainder launch (nsteps = iterations % T) runs the
@@ -570,7 +578,8 @@ class Hotspot(Problem):
             assert nsteps == self.iterations % cfg["temporal_tiling_factor"], nsteps
             kernel = self._rem_kernel(kernel, smem)
         return Launch(kernel, grid, block, [C.c_uint64(int(dst)), C.c_uint64(int(src)), C.c_uint64(int(power)),
-                                            C.c_int(nsteps)] + self._coeff_args() + extra, smem=smem)
+                                            C.c_int(nsteps)] + self._coeff_args() + extra, smem=smem,
+                      pdl=bool(extra) and pdl and self.STREAM_PDL)
 
     @staticmethod
     def _rem_kernel(kernel, smem: int):
@@ -589,8 +598,10 @@ class Hotspot(Problem):
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         plan = self.step_plan(cfg["temporal_tiling_factor"])
         shape = self.launch_shape(cfg, kernel)
+        # launches 2..n of a run: programmatic dependent launch (stream
+        # kernels wait on griddepcontrol before reading the previous output)
         return self._chain(kernel, bufs, len(plan), lambda i, s, d: self.launch(
-            cfg, kernel, d.ptr, s.ptr, bufs["power"].ptr, plan[i], shape))
+            cfg, kernel, d.ptr, s.ptr, bufs["power"].ptr, plan[i], shape, pdl=i > 0))
 
     def reference_launches(self, kernel, bufs: dict) -> list:
         from .runtime import Launch

@@ -33,6 +33,7 @@ class LaunchT(C.Structure):
         ("block", C.c_uint * 3),
         ("cluster", C.c_uint * 3),
         ("smem_bytes", C.c_uint),
+        ("flags", C.c_uint),  # TSG_LAUNCH_PDL
         ("args", C.POINTER(C.c_void_p)),
     ]
 
@@ -114,6 +115,7 @@ SIGNATURES = {
 }
 
 SLOTS = 16  # include/tsgpu.h TSG_SLOTS (pipelined submission slots)
+LAUNCH_PDL = 1  # include/tsgpu.h TSG_LAUNCH_PDL
 
 _lib = None
 _lib_lock = threading.Lock()
@@ -291,12 +293,13 @@ class Launch:
     c_int / c_float for values); they are kept alive by this object.
     """
 
-    def __init__(self, kernel: Kernel, grid, block, args, smem: int = 0, cluster=(1, 1, 1)):
+    def __init__(self, kernel: Kernel, grid, block, args, smem: int = 0, cluster=(1, 1, 1), pdl: bool = False):
         self.kernel = kernel
         self.grid = tuple(int(g) for g in grid) + (1,) * (3 - len(grid))
         self.block = tuple(int(b) for b in block) + (1,) * (3 - len(block))
         self.cluster = tuple(int(c) for c in cluster) + (1,) * (3 - len(cluster))
         self.smem = int(smem)
+        self.pdl = bool(pdl)  # programmatic dependent launch (kernel runs griddepcontrol.wait)
         self.args = list(args)
         self._ptrs = (C.c_void_p * max(1, len(self.args)))(
             *[C.cast(C.pointer(a), C.c_void_p) for a in self.args])
@@ -308,6 +311,7 @@ class Launch:
         s.block[:] = self.block
         s.cluster[:] = self.cluster
         s.smem_bytes = self.smem
+        s.flags = LAUNCH_PDL if self.pdl else 0
         s.args = C.cast(self._ptrs, C.POINTER(C.c_void_p))
         return s
 
