@@ -76,9 +76,20 @@ def build_oracle() -> None:
         _run(["make", "-s", "-C", str(oracle)])
 
 
+def install_reference() -> None:
+    """The UNMODIFIED reference under baseline/_ref (git-ignored, travels to
+    the GPU box with the snapshot) for bench.py's reference arm -- only where
+    /root/reference exists (this container), only if missing."""
+    recipe = ROOT / "baseline" / "install_reference.sh"
+    if (Path("/root/reference/pkg").is_dir() and recipe.exists()
+            and not (ROOT / "baseline" / "_ref" / "tunescape" / "__init__.py").exists()):
+        _run(["bash", str(recipe)])
+
+
 def build_all(force: bool = False, kernels: bool = True) -> None:
     build_libtsgpu(force)
     build_oracle()
+    install_reference()
     if kernels:
         check_kernels()
 

@@ -6,27 +6,34 @@
 //
 //   a(m,k) = Ak[m*GK + k]   b(k,n) = Bk[n*GK + k]   c(m,n) = C[n*GM + m]
 //
-// One CTA computes a BM x BN = 128 x BN_T tile (BN_T in {128, 256}):
+// PERSISTENT kernel: one CTA per SM (or one 2-CTA cluster per SM pair)
+// loops over work items -- 128 x BN_T output tiles (BN_T in {128, 256}),
+// and, for the tiles that would form a partial last wave, half tiles of
+// 128 x BN_T/2 -- assigned round-robin (item = cta + i * ncta).  Warp roles:
 //   warp 0      TMA producer: per k-block of BK=32 one A box (32 K x 128 M)
 //               and one B box (32 K x BN_T N), 128B swizzle (K-major
 //               canonical: 128-B rows, 8-row / 1 KB atoms), into a
-//               STAGES-deep ring guarded by full/empty mbarriers
+//               STAGES-deep ring guarded by full/empty mbarriers; it runs
+//               straight on into the next item's k-blocks
 //   warp 1      TMEM allocator + single-thread MMA issuer:
 //               tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN_T, K=8,
-//               4 per k-block, accumulator in TMEM (BN_T fp32 columns);
-//               tcgen05.commit frees the smem stage / signals the epilogue
+//               4 per k-block, into one of TWO TMEM accumulators (2 x BN_T
+//               fp32 columns): item i accumulates in buffer i & 1 while the
+//               epilogue drains buffer (i-1) & 1 -- the tensor pipe never
+//               waits for an epilogue; tcgen05.commit frees smem stages and
+//               signals "accumulator full"
 //   warps 2-5   epilogue: tcgen05.ld 32x32b (TMEM lane = m) -> registers
-//               -> coalesced column stores of C (m contiguous)
+//               -> coalesced column stores of C (m contiguous), then one
+//               arrival per warp on the buffer's "accumulator empty" barrier
 // CLUSTER == 2: a 2-CTA thread-block cluster shares the B tile -- the two
 // CTAs own consecutive M tiles of the same N tile; each TMA-loads its own
 // A box and HALF of the B box, multicast into both CTAs' stage buffers
 // (cp.async.bulk.tensor ... .multicast::cluster), so L2->SM operand traffic
-// per output drops from (128+BN_T) to (128+BN_T/2) rows per k-block (the
-// single-CTA kernel is bound by it: ~18 TB/s of TMA reads, ncu
-// profiles/round2/ncu/ncu_gemm_tc_256-2.md).  A stage may be refilled only
-// when BOTH CTAs' MMAs have consumed it: every MMA commit arrives on the
-// empty barrier of both CTAs (tcgen05.commit ... .multicast::cluster), whose
-// count is 2.
+// per output drops from (128+BN_T) to (128+BN_T/2) rows per k-block.  A
+// stage may be refilled only when BOTH CTAs' MMAs have consumed it: every
+// MMA commit arrives on the empty barrier of both CTAs (tcgen05.commit ...
+// .multicast::cluster), whose count is 2.  Both CTAs of a cluster walk the
+// same item sequence, so their k-block counters stay in lock step.
 // Tunables (compile-time): BN_T, STAGES, CLUSTER.  Problem macros: GM, GN, GK.
 // Precision: operands are read as TF32 (10-bit mantissa) by the tensor
 // core, accumulation is fp32; verification uses a K-scaled tolerance.
@@ -47,7 +54,7 @@
 #define B_STAGE_BYTES (BN_T * BK * 4)
 #define STAGE_BYTES (A_STAGE_BYTES + B_STAGE_BYTES)
 #define NUM_THREADS 192
-#define TMEM_COLS BN_T
+#define TMEM_COLS (2 * BN_T)  // two accumulators
 
 struct __align__(64) TmaDesc {
   unsigned long long v[16];
@@ -149,47 +156,51 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
+// work item -> this CTA's output origin (m0, n0); see the kernel comment
+__device__ __forceinline__ void gemm_tc_item(int item, int n_full, int tiles_m, unsigned crank, int& m0, int& n0) {
+  const int tile = item < n_full ? item : n_full + ((item - n_full) >> 1);
+  const int half = item < n_full ? 0 : ((item - n_full) & 1);
+#if CLUSTER == 2
+  const int pairs_m = tiles_m >> 1;  // a cluster owns M tiles (2p, 2p+1) of one N tile
+  m0 = ((tile % pairs_m) * 2 + (int)crank) * BM;
+  n0 = (tile / pairs_m) * BN_T + half * (BN_T / 2);
+#else
+  (void)crank;
+  m0 = (tile % tiles_m) * BM;
+  n0 = (tile / tiles_m) * BN_T + half * (BN_T / 2);
+#endif
+}
+
 extern "C" __global__ void __launch_bounds__(NUM_THREADS, 1)
 gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
-               const __grid_constant__ TmaDesc tma_b, int tiles_m, int n_full) {
+               const __grid_constant__ TmaDesc tma_b, int tiles_m, int n_full, int n_items) {
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the 128B-swizzle atoms
   const unsigned base = smem_u32(smem_raw);
   const unsigned pad = (1024u - (base & 1023u)) & 1023u;
-  unsigned char* smem = smem_raw + pad;
   const unsigned sbase = base + pad;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + STAGES * STAGE_BYTES);
-  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * STAGES + 1);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem_raw + pad + STAGES * STAGE_BYTES);
+  unsigned* tmem_slot = reinterpret_cast<unsigned*>(bars + 2 * STAGES + 4);
   const unsigned full0 = smem_u32(bars);
   const unsigned empty0 = full0 + 8 * STAGES;
-  const unsigned tfull = full0 + 16 * STAGES;
+  const unsigned tfull0 = full0 + 16 * STAGES;   // accumulator full [2]
+  const unsigned tempty0 = tfull0 + 16;          // accumulator empty [2]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  // Work items (1-D grid): the first n_full are whole BM x BN_T tiles; the
-  // tiles after them (which would form a partial last wave over the SMs)
-  // are split into two BM x BN_T/2 halves each, so the last wave is as full
-  // as the others (512 whole tiles on 148 SMs would cap at 86.5%).  A half
-  // tile still TMA-loads a full BN_T-row B box (rows past its own 128 are
-  // unused / zero-filled past GN) and runs the MMA with N = BN_T/2.
+  // work-item walk: CTA (CLUSTER == 1) or cluster (CLUSTER == 2) `unit`
+  // takes items unit, unit + nunits, ...  Items < n_full are whole tiles
+  // (pairs of M tiles for CLUSTER == 2), the rest halves of the remaining
+  // tiles along N (a half still loads a full B box; rows past it unused).
 #if CLUSTER == 2
-  // a cluster owns M tiles (2p, 2p+1) of one N tile; whole tiles only
   const unsigned crank = cluster_rank();
-  const int pair = blockIdx.x >> 1;
-  const int pairs_m = tiles_m >> 1;
-  const int m0 = ((pair % pairs_m) * 2 + (int)crank) * BM;
-  const int bn = BN_T;
-  const int n0 = (pair / pairs_m) * BN_T;
-  (void)n_full;
+  const int unit = blockIdx.x >> 1;
+  const int nunits = gridDim.x >> 1;
 #else
-  const int item = blockIdx.x;
-  const int tile = item < n_full ? item : n_full + ((item - n_full) >> 1);
-  const int half = item < n_full ? -1 : ((item - n_full) & 1);
-  const int m0 = (tile % tiles_m) * BM;
-  const int bn = half < 0 ? BN_T : BN_T / 2;
-  const int n0 = (tile / tiles_m) * BN_T + (half > 0 ? BN_T / 2 : 0);
+  const unsigned crank = 0;
+  const int unit = blockIdx.x;
+  const int nunits = gridDim.x;
 #endif
-  const unsigned idesc = IDESC_N(bn);
   constexpr int KB = GK / BK;
 
   if (warp == 0 && lane == 0) {
@@ -197,7 +208,10 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
       mbar_init(full0 + 8 * s, 1);
       mbar_init(empty0 + 8 * s, CLUSTER);  // every CTA of the cluster releases the stage
     }
-    mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull0 + 8 * b, 1);   // MMA commit
+      mbar_init(tempty0 + 8 * b, 4);  // one arrival per epilogue warp
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tma_a)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<unsigned long long>(&tma_b)) : "memory");
@@ -217,96 +231,88 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
 
   if (warp == 0) {
     if (lane == 0) {  // ---- TMA producer
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES;
-        const unsigned ph = (kb / STAGES) & 1;
-        mbar_wait(empty0 + 8 * s, ph ^ 1);
-        const unsigned full = full0 + 8 * s;
-        mbar_expect_tx(full, STAGE_BYTES);
-        const unsigned sa = sbase + s * STAGE_BYTES;
-        const unsigned sb = sa + A_STAGE_BYTES;
-        tma_load_2d(sa, &tma_a, kb * BK, m0, full);  // coords: (k, m)
+      int g = 0;  // k-blocks issued so far (stage / phase)
+      for (int item = unit; item < n_items; item += nunits) {
+        int m0, n0;
+        gemm_tc_item(item, n_full, tiles_m, crank, m0, n0);
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(empty0 + 8 * s, ((g / STAGES) & 1) ^ 1);
+          const unsigned full = full0 + 8 * s;
+          mbar_expect_tx(full, STAGE_BYTES);
+          const unsigned sa = sbase + s * STAGE_BYTES;
+          const unsigned sb = sa + A_STAGE_BYTES;
+          tma_load_2d(sa, &tma_a, kb * BK, m0, full);  // coords: (k, m)
 #if CLUSTER == 2
-        // this CTA's half of the B box, into both CTAs (same offset)
-        tma_load_2d_mc(sb + crank * (B_STAGE_BYTES / 2), &tma_b, kb * BK, n0 + (int)crank * (BN_T / 2), full,
-                       (unsigned short)0x3);
+          // this CTA's half of the B box, into both CTAs (same offset)
+          tma_load_2d_mc(sb + crank * (B_STAGE_BYTES / 2), &tma_b, kb * BK, n0 + (int)crank * (BN_T / 2), full,
+                         (unsigned short)0x3);
 #else
-        tma_load_2d(sb, &tma_b, kb * BK, n0, full);  // coords: (k, n)
+          tma_load_2d(sb, &tma_b, kb * BK, n0, full);  // coords: (k, n)
 #endif
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer (single thread)
-      for (int kb = 0; kb < KB; ++kb) {
-        const int s = kb % STAGES;
-        const unsigned ph = (kb / STAGES) & 1;
-        mbar_wait(full0 + 8 * s, ph);
+      int g = 0, it = 0;
+      for (int item = unit; item < n_items; item += nunits, ++it) {
+        const int buf = it & 1;
+        const unsigned idesc = IDESC_N(item < n_full ? BN_T : BN_T / 2);
+        const unsigned acc = tmem + (unsigned)(buf * BN_T);
+        mbar_wait(tempty0 + 8 * buf, ((it >> 1) & 1) ^ 1);  // epilogue drained this buffer
         asm volatile("tcgen05.fence::after_thread_sync;");
-#ifdef DEBUG_DUMP_SMEM
-        if (kb == 0 && blockIdx.x == 0 && blockIdx.y == 0) {
-          const unsigned* w = reinterpret_cast<const unsigned*>(smem);
-          for (int i = 0; i < STAGE_BYTES / 4; ++i) reinterpret_cast<unsigned*>(C)[i] = w[i];
-        }
-#endif
-        const unsigned sa = sbase + s * STAGE_BYTES;
-        const unsigned sb = sa + A_STAGE_BYTES;
+        for (int kb = 0; kb < KB; ++kb, ++g) {
+          const int s = g % STAGES;
+          mbar_wait(full0 + 8 * s, (g / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const unsigned sa = sbase + s * STAGE_BYTES;
+          const unsigned sb = sa + A_STAGE_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / KSTEP; ++k) {
-          // K step of 8 tf32 = 32 bytes along the swizzled 128-byte rows
-          const unsigned long long da = umma_desc(sa + k * 32, 16, 1024);
-          const unsigned long long db = umma_desc(sb + k * 32, 16, 1024);
-#ifndef NO_MMA
-          umma_tf32(tmem, da, db, idesc, (kb | k) != 0);
+          for (int k = 0; k < BK / KSTEP; ++k) {
+            // K step of 8 tf32 = 32 bytes along the swizzled 128-byte rows
+            const unsigned long long da = umma_desc(sa + k * 32, 16, 1024);
+            const unsigned long long db = umma_desc(sb + k * 32, 16, 1024);
+            umma_tf32(acc, da, db, idesc, (kb | k) != 0);
+          }
+#if CLUSTER == 2
+          umma_commit_mc(empty0 + 8 * s, (unsigned short)0x3);  // releases the stage in both CTAs
 #else
-          (void)da;
-          (void)db;
+          umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs retire
 #endif
         }
-#if CLUSTER == 2
-        umma_commit_mc(empty0 + 8 * s, (unsigned short)0x3);  // releases the stage in both CTAs
-#else
-        umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs retire
-#endif
+        umma_commit(tfull0 + 8 * buf);  // accumulator complete
       }
-      umma_commit(tfull);  // accumulator complete
     }
   } else {
     // ---- epilogue: warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
-#ifdef DEBUG_TMEM_ST
-    {  // write a known pattern into TMEM, skip waiting for the MMAs
-      const unsigned ta = tmem + ((unsigned)(q * 32) << 16);
-      for (int c = 0; c < BN_T; ++c) {
-        unsigned val = __float_as_uint((float)((q * 32 + lane) * 1000 + c));
-        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(ta + c), "r"(val));
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-#else
-    mbar_wait(tfull, 0);
-#endif
-    asm volatile("tcgen05.fence::after_thread_sync;");
-#ifdef DEBUG_TMEM_ADDR
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 64) {
-      C[0] = __uint_as_float(tmem);
-    }
-    if (blockIdx.x == 0 && blockIdx.y == 0) return;
-#endif
-    const int m = m0 + q * 32 + lane;
-    const unsigned taddr = tmem + ((unsigned)(q * 32) << 16);
+    int it = 0;
+    for (int item = unit; item < n_items; item += nunits, ++it) {
+      const int buf = it & 1;
+      int m0, n0;
+      gemm_tc_item(item, n_full, tiles_m, crank, m0, n0);
+      const int bn = item < n_full ? BN_T : BN_T / 2;
+      mbar_wait(tfull0 + 8 * buf, (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int m = m0 + q * 32 + lane;
+      const unsigned taddr = tmem + ((unsigned)(q * 32) << 16) + (unsigned)(buf * BN_T);
 #pragma unroll 1
-    for (int c = 0; c < bn; c += 16) {
-      unsigned r[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-          : "r"(taddr + c));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#ifndef DEBUG_DUMP_SMEM
+      for (int c = 0; c < bn; c += 16) {
+        unsigned r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr + c));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 16; ++j) C[(size_t)(n0 + c + j) * GM + m] = __uint_as_float(r[j]);
-#endif
+        for (int j = 0; j < 16; ++j) C[(size_t)(n0 + c + j) * GM + m] = __uint_as_float(r[j]);
+      }
+      // this warp's TMEM reads are complete: hand the buffer back to the MMA issuer
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(tempty0 + 8 * buf) : "memory");
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

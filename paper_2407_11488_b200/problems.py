@@ -1006,7 +1006,8 @@ class GemmTC(Gemm):
     kernel_name = "gemm_tc_kernel"
     reference_kernel = "gemm_reference"
 
-    def __init__(self, m: int = 4096, n: int = 4096, k: int = 4096, seed_a: int = 6, seed_b: int = 7):
+    def __init__(self, m: int = 4096, n: int = 4096, k: int = 4096, seed_a: int = 6, seed_b: int = 7,
+                 max_units: int | None = None):
         from .paramspace import space_from_tune_params
 
         self.space = space_from_tune_params(
@@ -1016,6 +1017,7 @@ class GemmTC(Gemm):
         self._host = None
         self.M, self.N, self.K = m, n, k
         self.seed_a, self.seed_b = seed_a, seed_b
+        self.max_units = max_units  # cap on the persistent grid (tests: several items per CTA)
         # K-scaled tf32 bound: |dC| <= c*K*eps*max|a|*max|b|, eps = 2^-11, c = 1
         self.abs_tol = self.K * 2.0 ** -11
         self.rtol = 1.0  # the norm-wise check is replaced by abs_tol
@@ -1036,7 +1038,9 @@ class GemmTC(Gemm):
                 BufferSpec("out", self.M * self.N * 4)]
 
     def smem_bytes(self, cfg: dict) -> int:
-        return cfg["STAGES"] * (16384 + cfg["BN_T"] * 128) + 1024 + 256
+        # >= 116 KiB: one CTA per SM (a second CTA's 2 x BN_T TMEM columns
+        # would wait for the first to finish anyway)
+        return max(cfg["STAGES"] * (16384 + cfg["BN_T"] * 128) + 1024 + 256, 116 * 1024)
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
@@ -1049,16 +1053,17 @@ class GemmTC(Gemm):
         tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"] // cluster, 128)
         tiles_m = self.M // 128
         tiles = tiles_m * (self.N // cfg["BN_T"])
-        if cluster == 2:
-            return [Launch(kernel, (tiles, 1, 1), (192, 1, 1),
-                           [_u64(bufs["out"]), ta, tb, C.c_int(tiles_m), C.c_int(tiles)],
-                           smem=self.smem_bytes(cfg), cluster=(2, 1, 1))]
+        # persistent: one CTA (cluster == 1) or one 2-CTA cluster per SM
+        # (pair); work units = whole tiles (pairs of M tiles for clusters)
+        # while they fill whole waves of the persistent grid, then halves
         n_sm = int(dev.info.get("sm_count", 148))
-        n_full = (tiles // n_sm) * n_sm  # whole waves of whole tiles; the rest run as halves
-        items = n_full + 2 * (tiles - n_full)
-        return [Launch(kernel, (items, 1, 1), (192, 1, 1),
-                       [_u64(bufs["out"]), ta, tb, C.c_int(tiles_m), C.c_int(n_full)],
-                       smem=self.smem_bytes(cfg))]
+        units = tiles // cluster
+        n_units = min(n_sm // cluster, units, self.max_units or units)
+        n_full = (units // n_units) * n_units
+        items = n_full + 2 * (units - n_full)
+        return [Launch(kernel, (n_units * cluster, 1, 1), (192, 1, 1),
+                       [_u64(bufs["out"]), ta, tb, C.c_int(tiles_m), C.c_int(n_full), C.c_int(items)],
+                       smem=self.smem_bytes(cfg), cluster=(cluster, 1, 1))]
 
 
 PROBLEMS = {"convolution": Convolution, "hotspot": Hotspot, "dedispersion": Dedispersion,

@@ -196,19 +196,22 @@ def test_gemm_tc_tf32_within_k_scaled_tolerance(device):
     """tcgen05/TMEM/TMA tf32 GEMM vs the fp32 oracle: |dC| <= K * 2^-11 (|a|,|b| <= 1)."""
     from paper_2407_11488_b200.problems import GemmTC
 
-    prob = GemmTC(m=512, n=512, k=384)
-    want = K.answer(prob)
-    tgt = CudaTarget(prob, device=device, answer=want)
-    try:
-        for c in prob.space.enumerate_configs():
-            obs = tgt.execute(c, PROTO)
-            assert obs.ok, (c, obs)
-            st, out = tgt.run_output(c)
-            err = float(np.max(np.abs(out.astype(np.float64) - want)))
-            assert err <= prob.K * 2.0 ** -11, (c, err)
-            assert err > 0  # it really is tf32, not a silent fp32 path
-    finally:
-        tgt.close()
+    # the persistent grid capped at 3 CTAs / clusters: every CTA walks several
+    # whole and half tiles through both TMEM accumulators
+    for max_units in (None, 3):
+        prob = GemmTC(m=512, n=512, k=384, max_units=max_units)
+        want = K.answer(prob)
+        tgt = CudaTarget(prob, device=device, answer=want)
+        try:
+            for c in prob.space.enumerate_configs():
+                obs = tgt.execute(c, PROTO)
+                assert obs.ok, (max_units, c, obs)
+                st, out = tgt.run_output(c)
+                err = float(np.max(np.abs(out.astype(np.float64) - want)))
+                assert err <= prob.K * 2.0 ** -11, (max_units, c, err)
+                assert err > 0  # it really is tf32, not a silent fp32 path
+        finally:
+            tgt.close()
     big = GemmTC()
     tgt = CudaTarget(big, device=device)
     try:
