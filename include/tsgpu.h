@@ -63,8 +63,8 @@ typedef struct tsg_kernel tsg_kernel;
  * {1,1,1} means no cluster launch.  flags: TSG_LAUNCH_PDL launches with
  * programmatic stream serialization (the kernel may be scheduled while the
  * previous kernel in the stream drains; it must execute
- * griddepcontrol.wait before touching that kernel's results).  The field
- * occupies what was padding before `args`: the layout is unchanged. */
+ * griddepcontrol.wait before touching that kernel's results; round 2 --
+ * the field moved `args` from offset 48 to 56). */
 #define TSG_LAUNCH_PDL 1u
 typedef struct {
   tsg_kernel* fn;

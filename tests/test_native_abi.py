@@ -75,3 +75,22 @@ def test_init_without_driver_is_a_clean_error():
         pytest.skip("a GPU is present on this host")
     assert rc == rt.ERR_SETUP
     assert rt.last_error()
+
+
+def test_launch_record_layout_matches_header():
+    """tsg_launch_t (include/tsgpu.h): the ctypes mirror has the header's
+    field order and offsets (`flags`, TSG_LAUNCH_PDL, sits between
+    `smem_bytes` and `args`)."""
+    import ctypes as C
+    import re
+    from pathlib import Path
+
+    from paper_2407_11488_b200.runtime import LAUNCH_PDL, LaunchT
+
+    hdr = (Path(__file__).resolve().parents[1] / "include" / "tsgpu.h").read_text()
+    body = re.search(r"typedef struct \{([^}]*)\} tsg_launch_t;", hdr).group(1)
+    names = re.findall(r"(\w+)(?:\[\d\])?;", body)
+    assert names == [f[0] for f in LaunchT._fields_]
+    assert int(re.search(r"#define TSG_LAUNCH_PDL (\d+)u", hdr).group(1)) == LAUNCH_PDL
+    assert LaunchT.smem_bytes.offset == 44 and LaunchT.flags.offset == 48
+    assert LaunchT.args.offset == 56 and C.sizeof(LaunchT) == 64
