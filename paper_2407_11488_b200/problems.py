@@ -453,6 +453,8 @@ class Hotspot(Problem):
     # programmatic dependent launch between the launches of one run
     # (TSG_HS_PDL=0 disables it for experiments)
     STREAM_PDL = os.environ.get("TSG_HS_PDL", "1") != "0"
+    # experiments: cap the warps per SM the segment geometry assumes
+    STREAM_WARPS_CAP = int(os.environ.get("TSG_HS_WARPS_CAP", "0"))
 
     def _segments(self, nsegs: int) -> tuple:
         """(segh, segh0, nsegs): interior and first segment heights, segment count.
@@ -557,6 +559,8 @@ class Hotspot(Problem):
             occ = getattr(kernel, "occupancy", None)
             if occ is not None:
                 bps = occ(cfg["block_size_x"] * cfg["block_size_y"], geo["smem"])
+                if self.STREAM_WARPS_CAP:  # experiments: fewer, taller segments
+                    bps = min(bps, max(1, self.STREAM_WARPS_CAP // geo["wpb"]))
                 geo = self.stream_geometry(cfg, blocks_per_sm=max(1, bps), n_sm=kernel.sm_count)
             return (geo["blocks"], 1, 1), block, geo["smem"], [
                 C.c_int(geo[k]) for k in ("segh", "nsegs", "segh0", "seghe", "nsegse", "segh0e")]
