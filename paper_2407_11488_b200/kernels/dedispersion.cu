@@ -284,6 +284,21 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
     dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
     const float* srow = smem + stg * CC * ROWLEN + lane;
     const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
+#ifdef DD_PF
+    // software-pipelined: channel c+1's packed offset/case is shuffled out
+    // while channel c's case runs (the shuffle latency leaves the chain)
+    int pk = __shfl_sync(0xffffffffu, mine, 0);
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c, srow += ROWLEN) {
+      const int pkn = __shfl_sync(0xffffffffu, mine, (c + 1) & 31);
+#ifdef DD_HAVE_ASM
+      dd_asm_dispatch(acc, pk & 0xff, dd_smem_u32(srow + (pk >> 8)));
+#else
+      dd_dispatch(st, pk & 0xff, srow + (pk >> 8));
+#endif
+      pk = pkn;
+    }
+#else
 #pragma unroll 1
     for (int c = 0; c < nch; ++c, srow += ROWLEN) {
       const int pk = __shfl_sync(0xffffffffu, mine, c);
@@ -293,6 +308,7 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       dd_dispatch(st, pk & 0xff, srow + (pk >> 8));
 #endif
     }
+#endif
     // release the stage: one arrival per warp; the producer (warp 0) refills
     // it once all warps have arrived -- the other warps run ahead on the
     // stages already in flight instead of meeting at a block barrier

@@ -76,3 +76,47 @@ def test_gpu_dedispersion_cache_imports_into_reference(tmp_path, reference_pkg):
     ref = ref_import(_unzip("dedispersion.kerneltuner.json", tmp_path), expected_space=rs)
     assert len(ref.records) == 11130
     assert build_ffg(ref, rs) is not None  # complete landscape
+
+
+# ---- round 2: the hotspot (and, once swept, GEMM) spaces -------------------
+CACHES2 = Path(__file__).resolve().parents[1] / "profiles" / "round2" / "caches"
+FULL2 = {"hotspot": 105412, "gemm": 116928}
+
+
+def _unzip2(name: str, tmp_path: Path) -> Path:
+    p = tmp_path / name
+    p.write_bytes(gzip.decompress((CACHES2 / (name + ".gz")).read_bytes()))
+    return p
+
+
+def _swept(problem: str) -> bool:
+    return (CACHES2 / f"{problem}.tunescape.json.gz").exists()
+
+
+@pytest.mark.parametrize("problem", sorted(FULL2))
+def test_round2_full_space_cache(problem, tmp_path, reference_pkg):
+    """A whole reference space swept on a B200 through the tune command line
+    (every configuration verified on the device): complete in our format,
+    the Kernel-Tuner export imports into the UNMODIFIED reference with
+    ``expected_space`` and its ``build_ffg`` (IncompleteCache otherwise)
+    builds the complete landscape; the summary's best is the cache's best."""
+    if not _swept(problem):
+        pytest.skip(f"{problem}: full-space sweep not committed")
+    from tunescape.landscape import build_ffg
+    from tunescape.paramspace import bundled_space as ref_space
+    from tunescape.store import import_external_cache as ref_import
+
+    space = bundled_space(problem)
+    keys = {config_key(c) for c in space.enumerate_configs()}
+    assert len(keys) == FULL2[problem]
+    native = loads_cache(_unzip2(f"{problem}.tunescape.json", tmp_path).read_text())
+    assert set(native.records) == keys
+    ok = native.ok_records()
+    assert all(o.time_ms > 0 and len(o.times_ms) == 7 for o in ok.values())
+    summary = json.loads((CACHES2 / f"{problem}.summary.json").read_text())
+    best = min(ok.items(), key=lambda kv: kv[1].time_ms)
+    assert best[0] == ",".join(map(str, summary["best"])) and summary["ok"] == len(ok)
+    rs = ref_space(problem)
+    ref = ref_import(_unzip2(f"{problem}.kerneltuner.json", tmp_path), expected_space=rs)
+    assert len(ref.records) == len(keys)
+    assert build_ffg(ref, rs) is not None  # complete landscape
