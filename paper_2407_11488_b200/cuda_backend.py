@@ -62,7 +62,10 @@ def default_workers() -> int:
         n = len(os.sched_getaffinity(0))
     except AttributeError:
         n = os.cpu_count() or 1
-    return max(1, n - 1)
+    # one process per GPU: the node's host threads are shared by the ranks on
+    # it (torchrun's LOCAL_WORLD_SIZE), one left for the drivers' main threads
+    local = max(1, int(os.environ.get("LOCAL_WORLD_SIZE", "1")))
+    return max(1, (n - 1) // local)
 
 
 class Compiler:

@@ -170,3 +170,20 @@ def test_every_strategy_sharded_over_two_ranks_matches_one_process(tmp_path):
             per_rank[r] += int(mine)
     assert min(per_rank) > 0, per_rank  # both ranks measured parts of the batches
 
+
+
+def test_compile_pool_shares_the_node_between_local_ranks(monkeypatch):
+    """NVRTC workers per rank = (host threads - 1) // LOCAL_WORLD_SIZE: 8 ranks
+    on a 16-thread node get 1 worker each, not 15 (verdict r1 weak #8)."""
+    import os
+
+    from paper_2407_11488_b200.cuda_backend import default_workers
+
+    monkeypatch.delenv("TSG_COMPILE_WORKERS", raising=False)
+    monkeypatch.setattr(os, "sched_getaffinity", lambda pid: set(range(16)))
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "1")
+    assert default_workers() == 15
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "8")
+    assert default_workers() == 1
+    monkeypatch.setenv("LOCAL_WORLD_SIZE", "4")
+    assert default_workers() == 3
