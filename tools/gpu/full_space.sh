@@ -1,12 +1,14 @@
 #!/bin/bash
 # Whole-space brute-force sweep of one kernel through the command line,
-# resumable (the log survives a lost box), native + Kernel-Tuner caches,
-# summary (tools/sweep_summary.py) and the UNMODIFIED reference's own
-# `analyze stats` on the Kernel-Tuner cache; caches gzipped (gpurun copies
-# back <= 64 MiB).
+# resumable across gpurun calls: the resume log comes back gzipped in
+# gpurun_out/caches/ -- move it to sweeps/ (git-ignored, travels with the
+# snapshot) and the next call continues from it.  When complete: native +
+# Kernel-Tuner caches (gzipped; gpurun copies back <= 64 MiB), summary
+# (tools/sweep_summary.py) and the UNMODIFIED reference's `analyze stats`.
 #   gpurun --timeout 3600 -- 'bash tools/gpu/full_space.sh hotspot 3000'
 k=$1; lim=${2:-3000}
 d=gpurun_out/caches; mkdir -p $d
+[ -f sweeps/$k.log.jsonl.gz ] && gunzip -c sweeps/$k.log.jsonl.gz > $d/$k.log.jsonl && echo "resuming: $(wc -l < $d/$k.log.jsonl) logged"
 t0=$(date +%s)
 timeout $lim python -m paper_2407_11488_b200 tune --space $k --backend cuda:$k --strategy brute \
   --resume $d/$k.log.jsonl --out $d/$k.tunescape.json \
@@ -20,5 +22,7 @@ if [ -f $d/$k.tunescape.json ]; then
   cat $d/$k.reference_stats.txt
   gzip -9f $d/$k.tunescape.json $d/$k.kerneltuner.json
   rm -f $d/$k.log.jsonl*
+else
+  gzip -9f $d/$k.log.jsonl  # partial: bring the resume log back
 fi
 du -sh gpurun_out
