@@ -34,6 +34,13 @@
 // MMA commit arrives on the empty barrier of both CTAs (tcgen05.commit ...
 // .multicast::cluster), whose count is 2.  Both CTAs of a cluster walk the
 // same item sequence, so their k-block counters stay in lock step.
+// CLUSTER == 4: a 2 x 2 cluster owns 2 M tiles x 2 N tiles; CTA rank r is
+// (rm, rn) = (r & 1, r >> 1).  The two CTAs of an M tile each load half of
+// its A box and multicast it to both; the two CTAs of an N tile do the same
+// with B -- per CTA (64 + BN_T/2) rows per k-block instead of 128 + BN_T.
+// Every MMA commit arrives on the empty barrier of all four CTAs (count 4):
+// a stage is refilled only when every CTA that receives data into it has
+// consumed it.
 // Tunables (compile-time): BN_T, STAGES, CLUSTER.  Problem macros: GM, GN, GK.
 // Precision: operands are read as TF32 (10-bit mantissa) by the tensor
 // core, accumulation is fp32; verification uses a K-scaled tolerance.
@@ -160,7 +167,11 @@ __device__ __forceinline__ void cluster_sync_all() {
 __device__ __forceinline__ void gemm_tc_item(int item, int n_full, int tiles_m, unsigned crank, int& m0, int& n0) {
   const int tile = item < n_full ? item : n_full + ((item - n_full) >> 1);
   const int half = item < n_full ? 0 : ((item - n_full) & 1);
-#if CLUSTER == 2
+#if CLUSTER == 4
+  const int pairs_m = tiles_m >> 1;  // a cluster owns M tiles (2pm, 2pm+1) x N tiles (2pn, 2pn+1)
+  m0 = ((tile % pairs_m) * 2 + (int)(crank & 1)) * BM;
+  n0 = ((tile / pairs_m) * 2 + (int)(crank >> 1)) * BN_T + half * (BN_T / 2);
+#elif CLUSTER == 2
   const int pairs_m = tiles_m >> 1;  // a cluster owns M tiles (2p, 2p+1) of one N tile
   m0 = ((tile % pairs_m) * 2 + (int)crank) * BM;
   n0 = (tile / pairs_m) * BN_T + half * (BN_T / 2);
@@ -192,10 +203,10 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   // takes items unit, unit + nunits, ...  Items < n_full are whole tiles
   // (pairs of M tiles for CLUSTER == 2), the rest halves of the remaining
   // tiles along N (a half still loads a full B box; rows past it unused).
-#if CLUSTER == 2
+#if CLUSTER > 1
   const unsigned crank = cluster_rank();
-  const int unit = blockIdx.x >> 1;
-  const int nunits = gridDim.x >> 1;
+  const int unit = blockIdx.x / CLUSTER;
+  const int nunits = gridDim.x / CLUSTER;
 #else
   const unsigned crank = 0;
   const int unit = blockIdx.x;
@@ -223,8 +234,8 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-#if CLUSTER == 2
-  cluster_sync_all();  // the peer's barriers are initialised before anything targets them
+#if CLUSTER > 1
+  cluster_sync_all();  // the peers' barriers are initialised before anything targets them
 #endif
   asm volatile("tcgen05.fence::after_thread_sync;");
   const unsigned tmem = *tmem_slot;
@@ -242,12 +253,21 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
           mbar_expect_tx(full, STAGE_BYTES);
           const unsigned sa = sbase + s * STAGE_BYTES;
           const unsigned sb = sa + A_STAGE_BYTES;
+#if CLUSTER == 4
+          {  // half of the A box to the M-tile's two CTAs, half of the B box to the N-tile's two
+            const unsigned rm = crank & 1, rn = crank >> 1;
+            tma_load_2d_mc(sa + rn * (A_STAGE_BYTES / 2), &tma_a, kb * BK, m0 + (int)rn * (BM / 2), full,
+                           (unsigned short)((1u << rm) | (1u << (rm + 2))));
+            tma_load_2d_mc(sb + rm * (B_STAGE_BYTES / 2), &tma_b, kb * BK, n0 + (int)rm * (BN_T / 2), full,
+                           (unsigned short)(3u << (2 * rn)));
+          }
+#elif CLUSTER == 2
           tma_load_2d(sa, &tma_a, kb * BK, m0, full);  // coords: (k, m)
-#if CLUSTER == 2
           // this CTA's half of the B box, into both CTAs (same offset)
           tma_load_2d_mc(sb + crank * (B_STAGE_BYTES / 2), &tma_b, kb * BK, n0 + (int)crank * (BN_T / 2), full,
                          (unsigned short)0x3);
 #else
+          tma_load_2d(sa, &tma_a, kb * BK, m0, full);  // coords: (k, m)
           tma_load_2d(sb, &tma_b, kb * BK, n0, full);  // coords: (k, n)
 #endif
         }
@@ -275,8 +295,8 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
             const unsigned long long db = umma_desc(sb + k * 32, 16, 1024);
             umma_tf32(acc, da, db, idesc, (kb | k) != 0);
           }
-#if CLUSTER == 2
-          umma_commit_mc(empty0 + 8 * s, (unsigned short)0x3);  // releases the stage in both CTAs
+#if CLUSTER > 1
+          umma_commit_mc(empty0 + 8 * s, (unsigned short)((1u << CLUSTER) - 1));  // releases the stage in every CTA
 #else
           umma_commit(empty0 + 8 * s);  // frees the stage once these MMAs retire
 #endif
@@ -317,7 +337,7 @@ gemm_tc_kernel(float* __restrict__ C, const __grid_constant__ TmaDesc tma_a,
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-#if CLUSTER == 2
+#if CLUSTER > 1
   cluster_sync_all();  // no peer multicast or commit may still target this CTA's smem
 #endif
   if (warp == 1) {

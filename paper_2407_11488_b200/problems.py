@@ -1015,7 +1015,7 @@ class GemmTC(Gemm):
         from .paramspace import space_from_tune_params
 
         self.space = space_from_tune_params(
-            "gemm_tc", {"BN_T": [128, 256], "STAGES": [2, 3, 4, 5, 6], "CLUSTER": [1, 2]},
+            "gemm_tc", {"BN_T": [128, 256], "STAGES": [2, 3, 4, 5, 6], "CLUSTER": [1, 2, 4]},
             ["STAGES * (16384 + BN_T * 128) + 1280 <= 232448"],
             metric="(2 * 4096^3) / (time_ms * 1e6)")
         self._host = None
@@ -1052,9 +1052,10 @@ class GemmTC(Gemm):
         dev = bufs["Ak"].dev
         # K-major operands: dim0 = K (contiguous), dim1 = M / N; boxes of 32 K x (128 | BN_T)
         cluster = cfg.get("CLUSTER", 1)
-        ta = dev.tma_2d_f32(bufs["Ak"], self.K, self.M, self.K * 4, 32, 128, 128)
-        # cluster of 2: each CTA loads (and multicasts) half of the B box
-        tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"] // cluster, 128)
+        # cluster of 2: each CTA loads (and multicasts) half of the B box;
+        # 2 x 2 cluster: half of the A box and half of the B box
+        ta = dev.tma_2d_f32(bufs["Ak"], self.K, self.M, self.K * 4, 32, 128 // (2 if cluster == 4 else 1), 128)
+        tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"] // min(cluster, 2), 128)
         tiles_m = self.M // 128
         tiles = tiles_m * (self.N // cfg["BN_T"])
         # persistent: one CTA (cluster == 1) or one 2-CTA cluster per SM

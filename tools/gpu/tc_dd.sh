@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/tc_build.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu -k "gemm_tc" > gpurun_out/pytest_tc.log 2>&1
 tail -3 gpurun_out/pytest_tc.log
-timeout 600 python tools/run_configs.py gemm_tc "256,2,1;256,3,1;256,4,1;128,4,1;128,6,1;256,2,2;256,3,2;256,4,2;128,4,2;128,6,2" > gpurun_out/tc_times.jsonl 2> gpurun_out/tc_times.err
+timeout 600 python tools/run_configs.py gemm_tc --sample 24 --seed 1 > gpurun_out/tc_times.jsonl 2> gpurun_out/tc_times.err
 cat gpurun_out/tc_times.jsonl | python -c "
 import json,sys
 for l in sys.stdin:
