@@ -54,6 +54,15 @@ def main():
            "best_over_median": round(med / times[best], 3), "best_over_worst": round(times[worst] / times[best], 3),
            "by_mode": {m: {"n": len(v), "best_ms": round(min(v), 4), "median_ms": round(statistics.median(v), 4)}
                        for m, v in sorted(by.items())}}
+    # the paper's Table 4 metric per kernel: GFLOP/s for
+    # convolution / hotspot / GEMM, GB/s (4 B loaded per add) for dedispersion
+    if hasattr(prob, "paper_bytes"):
+        work, unit = prob.paper_bytes(), "GB/s"
+    else:
+        work, unit = prob.flops(), "GFLOP/s"
+    perf = sorted(work / (t * 1e6) for t in times.values())
+    doc["table4"] = {"unit": unit, "median": round(statistics.median(perf), 1), "maximum": round(perf[-1], 1),
+                     "impact": round(perf[-1] / statistics.median(perf), 2)}
     if a.wall_s:
         doc["wall_s"] = round(a.wall_s)
         doc["configs_per_s"] = round(len(cache.records) / a.wall_s, 2)
