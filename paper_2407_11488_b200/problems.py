@@ -1015,8 +1015,8 @@ class GemmTC(Gemm):
         from .paramspace import space_from_tune_params
 
         self.space = space_from_tune_params(
-            "gemm_tc", {"BN_T": [128, 256], "STAGES": [2, 3, 4, 5, 6], "CLUSTER": [1, 2, 4]},
-            ["STAGES * (16384 + BN_T * 128) + 1280 <= 232448"],
+            "gemm_tc", {"BN_T": [128, 256], "STAGES": [2, 3, 4, 5, 6], "CLUSTER": [1, 2]},
+            ["STAGES * (16384 + BN_T * 128 / CLUSTER) + 1280 <= 232448"],
             metric="(2 * 4096^3) / (time_ms * 1e6)")
         self._host = None
         self.M, self.N, self.K = m, n, k
@@ -1044,7 +1044,7 @@ class GemmTC(Gemm):
     def smem_bytes(self, cfg: dict) -> int:
         # >= 116 KiB: one CTA per SM (a second CTA's 2 x BN_T TMEM columns
         # would wait for the first to finish anyway)
-        return max(cfg["STAGES"] * (16384 + cfg["BN_T"] * 128) + 1024 + 256, 116 * 1024)
+        return max(cfg["STAGES"] * (16384 + cfg["BN_T"] * 128 // cfg.get("CLUSTER", 1)) + 1024 + 256, 116 * 1024)
 
     def launches(self, cfg: dict, kernel, bufs: dict) -> list:
         from .runtime import Launch
@@ -1052,10 +1052,9 @@ class GemmTC(Gemm):
         dev = bufs["Ak"].dev
         # K-major operands: dim0 = K (contiguous), dim1 = M / N; boxes of 32 K x (128 | BN_T)
         cluster = cfg.get("CLUSTER", 1)
-        # cluster of 2: each CTA loads (and multicasts) half of the B box;
-        # 2 x 2 cluster: half of the A box and half of the B box
-        ta = dev.tma_2d_f32(bufs["Ak"], self.K, self.M, self.K * 4, 32, 128 // (2 if cluster == 4 else 1), 128)
-        tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"] // min(cluster, 2), 128)
+        # 2-SM pair (cta_group::2): each CTA holds its own 128 A rows and half of the B tile
+        ta = dev.tma_2d_f32(bufs["Ak"], self.K, self.M, self.K * 4, 32, 128, 128)
+        tb = dev.tma_2d_f32(bufs["Bk"], self.K, self.N, self.K * 4, 32, cfg["BN_T"] // cluster, 128)
         tiles_m = self.M // 128
         tiles = tiles_m * (self.N // cfg["BN_T"])
         # persistent: one CTA (cluster == 1) or one 2-CTA cluster per SM
