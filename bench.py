@@ -85,7 +85,7 @@ KERNEL_SAMPLES = {
     "convolution": ([(256, 2, 4, 4, 1, 0, 0)], "tile_size_y", 11),
     "dedispersion": ([(32, 32, 4, 8, 1, 0)], "block_size_x", 7),
     "gemm": ([(128, 64, 16, 16, 8, 16, 8, 4, 4, 1, 1, 1, 1)], "VWM", 9),
-    "gemm_tc": ([(256, 2, 1), (256, 2, 2)], None, 6),
+    "gemm_tc": ([(256, 6, 2), (256, 4, 1)], None, 6),
 }
 
 
@@ -402,8 +402,13 @@ def kernels_block(dev, compiler, peaks, proto, seed) -> dict:
     from paper_2407_11488_b200.cuda_backend import CudaTarget
     from paper_2407_11488_b200.paramspace import config_key
     from paper_2407_11488_b200.problems import make_problem
-    from paper_2407_11488_b200.sweep import roofline, stratified_sample
+    from paper_2407_11488_b200.sweep import cublas_tf32, roofline, stratified_sample
 
+    if "gemm_tc" in KERNEL_SAMPLES and "cublas_tf32_tflops" not in peaks:
+        try:  # the library tf32 GEMM on the same shape (untimed; reported as roofline.alt)
+            peaks.update(cublas_tf32())
+        except Exception as e:  # noqa: BLE001 -- context only, never a denominator
+            peaks["cublas_tf32_error"] = str(e)[:200]
     out = {}
     for name, (known, param, n) in KERNEL_SAMPLES.items():
         t0 = time.perf_counter()
@@ -772,7 +777,11 @@ def our_arm(args, dist: Dist):
                       "fp32_source": "measured in-run: max of scalar FFMA and packed FFMA2 probes "
                                      "(kernels/peak.cu)",
                       "tf32_tflops": round(peaks["tf32_tflops"], 2) if peaks.get("tf32_tflops") else None,
-                      "tf32_source": peaks.get("tf32_source", peaks.get("tf32_error"))},
+                      "tf32_source": peaks.get("tf32_source", peaks.get("tf32_error")),
+                      "cublas_tf32_tflops": round(peaks["cublas_tf32_tflops"], 1)
+                      if peaks.get("cublas_tf32_tflops") else peaks.get("cublas_tf32_error"),
+                      "cublas_tf32_source": "in-run torch.matmul fp32 4096^3 with TF32 allowed (context for "
+                                            "the tcgen05 tf32 GEMM, never a denominator)"},
             "kernels": kernels,
             "e2e": e2e, "cpu_baseline": cpu, "gpu_launches": int(launches), "clocks": clocks,
             "setup_s": round(setup_s, 2), "wall_s_timed": round(wall_s, 3),

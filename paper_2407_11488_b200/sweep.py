@@ -109,6 +109,38 @@ def fp32_peak(dev: rt.Device, iters: int = 2048) -> dict:
     return r
 
 
+def cublas_tf32(n: int = 4096, reps: int = 10) -> dict:
+    """cuBLAS TF32 GEMM (torch.matmul on fp32, TF32 allowed) on the tuned
+    problem's shape, best of ``reps`` after warm-up, CUDA events: the library
+    baseline the tcgen05 kernel is compared with (bench `alt.vs_cublas`).
+    torch is plumbing here; the tuned kernels never go through it."""
+    import torch
+
+    if not torch.cuda.is_available():
+        return {}
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        a = torch.rand(n, n, device="cuda")
+        b = torch.rand(n, n, device="cuda")
+        for _ in range(3):
+            torch.matmul(a, b)
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            torch.matmul(a, b)
+            e.record()
+            e.synchronize()
+            best = min(best, s.elapsed_time(e))
+        del a, b
+        torch.cuda.empty_cache()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    return {"cublas_tf32_tflops": 2.0 * n ** 3 / (best * 1e-3) / 1e12, "cublas_tf32_ms": best}
+
+
 def tf32_peak(dev: rt.Device, iters: int = 4096) -> dict:
     """Dense tf32 tcgen05 throughput of this GPU (TFLOP/s), measured with CUDA
     events: kernels/peak.cu tf32_mma_peak, one CTA per SM issuing back-to-back
@@ -183,9 +215,12 @@ def roofline(problem, cfg: dict, info: dict, peaks: dict) -> dict:
         else:
             tf32, src = 0.5 * peaks.get("bf16_tflops", 1639.7), "0.5 x MEASURED_PEAKS bf16_tflops (fallback)"
         tfs = flop / t / 1e12
+        alt = {"hbm_gbs": round(byts / t / 1e9, 2)}
+        if peaks.get("cublas_tf32_tflops"):  # the library GEMM on the same problem, same run
+            alt["cublas_tf32_tflops"] = round(peaks["cublas_tf32_tflops"], 1)
+            alt["vs_cublas"] = round(tfs / peaks["cublas_tf32_tflops"], 3)
         return {"bound": "tensor", "achieved": round(tfs, 2), "peak": round(tf32, 2), "unit": "TFLOP/s",
-                "frac": round(tfs / tf32, 4), "traffic": None, "peak_source": src,
-                "alt": {"hbm_gbs": round(byts / t / 1e9, 2)}}
+                "frac": round(tfs / tf32, 4), "traffic": None, "peak_source": src, "alt": alt}
     fp32 = peaks.get("fp32_tflops", 0.0) * 1e12
     if getattr(problem, "space_name", "") == "dedispersion":
         # add-only kernel: the FP32 pipe retires one FADD per lane per cycle
