@@ -211,6 +211,12 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   unsigned long long* empty = bars + NSTAGE;
   float* sdelay = reinterpret_cast<float*>(empty + NSTAGE);
   unsigned char* pidx = reinterpret_cast<unsigned char*>(sdelay + NCH);
+#ifndef DD_NOSLOTS
+  // per-warp dispatch slots: for channel c of the current chunk, the case
+  // index and the warp-uniform byte address of its window in the staged row
+  // (one 8-byte broadcast LDS per channel replaces the shuffle + decode)
+  uint2* slots = reinterpret_cast<uint2*>(pidx + ((NPAT + 7) & ~7)) + threadIdx.y * 32;
+#endif
   // pattern -> dense case index (span-major, then value): a counting loop
   // (the constexpr dd_rank is recursive -- fine at compile time, a deep
   // call chain at run time)
@@ -281,24 +287,28 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       const int rel = sh0 - shb + ((sb + shb) & 3);  // offset from the aligned row start
       mine = (rel << 8) | pidx[pat];
     }
+#ifndef DD_NOSLOTS
+    // this lane's channel: case index + uniform window address (the lane's
+    // own sample is added per channel below)
+    slots[lane] = make_uint2((unsigned)(mine & 0xff),
+                             dd_smem_u32(smem + stg * CC * ROWLEN + lane * ROWLEN) + 4u * (unsigned)(mine >> 8));
+    __syncwarp();
+    dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
+    const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
+    const unsigned lane4 = 4u * (unsigned)lane;
+#pragma unroll 1
+    for (int c = 0; c < nch; ++c) {
+      const uint2 sl = slots[c];  // broadcast
+#ifdef DD_HAVE_ASM
+      dd_asm_dispatch(acc, (int)sl.x, sl.y + lane4);
+#else
+      dd_dispatch(st, (int)sl.x, reinterpret_cast<const float*>(__cvta_shared_to_generic(sl.y + lane4)));
+#endif
+    }
+#else
     dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
     const float* srow = smem + stg * CC * ROWLEN + lane;
     const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
-#ifdef DD_PF
-    // software-pipelined: channel c+1's packed offset/case is shuffled out
-    // while channel c's case runs (the shuffle latency leaves the chain)
-    int pk = __shfl_sync(0xffffffffu, mine, 0);
-#pragma unroll 1
-    for (int c = 0; c < nch; ++c, srow += ROWLEN) {
-      const int pkn = __shfl_sync(0xffffffffu, mine, (c + 1) & 31);
-#ifdef DD_HAVE_ASM
-      dd_asm_dispatch(acc, pk & 0xff, dd_smem_u32(srow + (pk >> 8)));
-#else
-      dd_dispatch(st, pk & 0xff, srow + (pk >> 8));
-#endif
-      pk = pkn;
-    }
-#else
 #pragma unroll 1
     for (int c = 0; c < nch; ++c, srow += ROWLEN) {
       const int pk = __shfl_sync(0xffffffffu, mine, c);
