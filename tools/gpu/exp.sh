@@ -1,12 +1,12 @@
 #!/bin/bash
-# Dedispersion experiment: time configs under TSG_EXTRA_DEFINES variants.
-#   gpurun -- 'bash tools/gpu/dd_exp.sh tag "cfg;cfg" "" "DD_PF=1" ...'
-tag=$1; cfgs=$2; shift 2
+# Time configurations of one problem under -D variants (TSG_EXTRA_DEFINES).
+#   gpurun -- 'bash tools/gpu/exp.sh dedispersion tag "cfg;cfg" "" "DD_NOSLOTS=1" ...'
+prob=$1; tag=$2; cfgs=$3; shift 3
 mkdir -p gpurun_out
-out=gpurun_out/dd_exp_$tag.jsonl; : > $out
+out=gpurun_out/exp_${prob}_$tag.jsonl; : > $out
 for v in "$@"; do
-  TSG_EXTRA_DEFINES="$v" timeout 900 python tools/run_configs.py dedispersion "$cfgs" --runs 7 \
-    2>>gpurun_out/dd_exp_$tag.err | sed "s/^{/{\"variant\": \"$v\", /" >> $out
+  TSG_EXTRA_DEFINES="$v" timeout 900 python tools/run_configs.py $prob "$cfgs" --runs 7 \
+    2>>gpurun_out/exp_${prob}_$tag.err | sed "s/^{/{\"variant\": \"$v\", /" >> $out
 done
 python - "$out" <<'PY'
 import json, sys, collections
