@@ -215,7 +215,9 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   // per-warp dispatch slots: for channel c of the current chunk, the case
   // index and the warp-uniform byte address of its window in the staged row
   // (one 8-byte broadcast LDS per channel replaces the shuffle + decode)
-  uint2* slots = reinterpret_cast<uint2*>(pidx + ((NPAT + 7) & ~7)) + threadIdx.y * 32;
+  // (16-byte aligned: pairs of slots are read as one uint4)
+  uint2* slots = reinterpret_cast<uint2*>((reinterpret_cast<size_t>(pidx + NPAT) + 15) & ~(size_t)15) +
+                 threadIdx.y * 32;
 #endif
   // pattern -> dense case index (span-major, then value): a counting loop
   // (the constexpr dd_rank is recursive -- fine at compile time, a deep
@@ -296,6 +298,20 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
     dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
     const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
     const unsigned lane4 = 4u * (unsigned)lane;
+#if defined(DD_HAVE_ASM) && !defined(DD_ONE)
+    // two channels (in order) per dispatch block: one slot load and one
+    // loop trip per pair
+    int c = 0;
+#pragma unroll 1
+    for (; c + 1 < nch; c += 2) {
+      const uint4 sl = *reinterpret_cast<const uint4*>(slots + c);  // broadcast
+      dd_asm_dispatch2(acc, (int)sl.x, sl.y + lane4, (int)sl.z, sl.w + lane4);
+    }
+    if (c < nch) {
+      const uint2 sl = slots[c];
+      dd_asm_dispatch(acc, (int)sl.x, sl.y + lane4);
+    }
+#else
 #pragma unroll 1
     for (int c = 0; c < nch; ++c) {
       const uint2 sl = slots[c];  // broadcast
@@ -305,6 +321,7 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       dd_dispatch(st, (int)sl.x, reinterpret_cast<const float*>(__cvta_shared_to_generic(sl.y + lane4)));
 #endif
     }
+#endif
 #else
     dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
     const float* srow = smem + stg * CC * ROWLEN + lane;

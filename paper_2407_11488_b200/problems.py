@@ -649,37 +649,45 @@ def dd_asm_dispatch(tsx: int, tsy: int, span: int) -> str:
     pats = sorted((p for p in range(1 << (tsy - 1)) if bin(p).count("1") <= span),
                   key=lambda p: (bin(p).count("1"), p))
     nacc = tsy * xp
-    idx_op, addr_op = nacc, nacc + 1
-    body = ["{", ".reg .f32 lo, hi;"]
-    body += [f".reg .b64 w{q}_{k};" for q in range(xp) for k in range(span + 1)]
-    body.append("ts_%=: .branchtargets " + ", ".join(f"L{i}_%=" for i in range(len(pats))) + ";")
-    body.append(f"brx.idx.uni %{idx_op}, ts_%=;")
-    for i, p in enumerate(pats):
-        body.append(f"L{i}_%=:")
-        ps = bin(p).count("1")
-        for q in range(xp):
-            for k in range(ps + 1):
-                body.append(f" ld.shared.f32 lo, [%{addr_op}+{4 * (64 * q + k)}];")
-                body.append(f" ld.shared.f32 hi, [%{addr_op}+{4 * (64 * q + 32 + k)}];")
-                body.append(f" mov.b64 w{q}_{k}, {{lo, hi}};")
-        for j in range(tsy):
-            g = bin(p & ((1 << j) - 1)).count("1")
+
+    def section(tag: str, idx_op: int, addr_op: int) -> list:
+        body = [f"ts{tag}_%=: .branchtargets " + ", ".join(f"L{tag}{i}_%=" for i in range(len(pats))) + ";",
+                f"brx.idx.uni %{idx_op}, ts{tag}_%=;"]
+        for i, p in enumerate(pats):
+            body.append(f"L{tag}{i}_%=:")
+            ps = bin(p).count("1")
             for q in range(xp):
-                a = j * xp + q
-                body.append(f" add.rn.f32x2 %{a}, %{a}, w{q}_{g};")
-        if i != len(pats) - 1:
-            body.append(" bra.uni D_%=;")
-    body.append("D_%=:")
-    body.append("}")
-    asm = "\\n".join(body)  # C string escapes: one PTX statement per line
+                for k in range(ps + 1):
+                    body.append(f" ld.shared.f32 lo, [%{addr_op}+{4 * (64 * q + k)}];")
+                    body.append(f" ld.shared.f32 hi, [%{addr_op}+{4 * (64 * q + 32 + k)}];")
+                    body.append(f" mov.b64 w{q}_{k}, {{lo, hi}};")
+            for j in range(tsy):
+                g = bin(p & ((1 << j) - 1)).count("1")
+                for q in range(xp):
+                    a = j * xp + q
+                    body.append(f" add.rn.f32x2 %{a}, %{a}, w{q}_{g};")
+            if i != len(pats) - 1:
+                body.append(f" bra.uni D{tag}_%=;")
+        body.append(f"D{tag}_%=:")
+        return body
+
+    head = ["{", ".reg .f32 lo, hi;"] + [f".reg .b64 w{q}_{k};" for q in range(xp) for k in range(span + 1)]
     outs = ", ".join(f'"+l"(acc[{j}][{q}])' for j in range(tsy) for q in range(xp))
+    one = "\\n".join(head + section("a", nacc, nacc + 1) + ["}"])  # C string escapes: one PTX statement per line
+    # two channels (in order) per asm block: the loop overhead and the
+    # dispatch-slot load are paid once per pair
+    two = "\\n".join(head + section("a", nacc, nacc + 1) + section("b", nacc + 2, nacc + 3) + ["}"])
     return (
         "#define DD_HAVE_ASM 1\n"
         "__device__ __forceinline__ void dd_asm_dispatch(unsigned long long (&acc)[TSY][XP], int idx, unsigned saddr) {\n"
         # volatile keeps it ordered after the (volatile) mbarrier wait; no
         # "memory" clobber, so the compiler may overlap the next channel's
-        # shuffle/decode with the adds
-        f'  asm volatile("{asm}" : {outs} : "r"(idx), "r"(saddr));\n'
+        # decode with the adds
+        f'  asm volatile("{one}" : {outs} : "r"(idx), "r"(saddr));\n'
+        "}\n"
+        "__device__ __forceinline__ void dd_asm_dispatch2(unsigned long long (&acc)[TSY][XP], int idx0, unsigned saddr0,"
+        " int idx1, unsigned saddr1) {\n"
+        f'  asm volatile("{two}" : {outs} : "r"(idx0), "r"(saddr0), "r"(idx1), "r"(saddr1));\n'
         "}\n")
 
 
@@ -810,7 +818,7 @@ class Dedispersion(Problem):
         npat = 1 << (cfg["tile_size_y"] - 1)
         slots = 8 * 32 * cfg["block_size_y"]  # per-warp dispatch slots (uint2 per channel)
         return (4 * self.DD_STAGES * self.DD_CC * rowlen + 16 * self.DD_STAGES + 4 * self.NCH
-                + ((npat + 7) & ~7) + slots)
+                + npat + 16 + slots)  # slots start 16-byte aligned after the pattern table
 
     # staged generic mode (kernels/dedispersion.cu DD_STG) for non-window
     # configurations with enough work per staged row: >= 4 threads and >= 12
