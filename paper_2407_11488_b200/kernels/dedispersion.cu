@@ -211,14 +211,6 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
   unsigned long long* empty = bars + NSTAGE;
   float* sdelay = reinterpret_cast<float*>(empty + NSTAGE);
   unsigned char* pidx = reinterpret_cast<unsigned char*>(sdelay + NCH);
-#ifndef DD_NOSLOTS
-  // per-warp dispatch slots: for channel c of the current chunk, the case
-  // index and the warp-uniform byte address of its window in the staged row
-  // (one 8-byte broadcast LDS per channel replaces the shuffle + decode)
-  // (16-byte aligned: pairs of slots are read as one uint4)
-  uint2* slots = reinterpret_cast<uint2*>((reinterpret_cast<size_t>(pidx + NPAT) + 15) & ~(size_t)15) +
-                 threadIdx.y * 32;
-#endif
   // pattern -> dense case index (span-major, then value): a counting loop
   // (the constexpr dd_rank is recursive -- fine at compile time, a deep
   // call chain at run time)
@@ -289,43 +281,25 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
       const int rel = sh0 - shb + ((sb + shb) & 3);  // offset from the aligned row start
       mine = (rel << 8) | pidx[pat];
     }
-#ifndef DD_NOSLOTS
-    // this lane's channel: case index + uniform window address (the lane's
-    // own sample is added per channel below)
-    slots[lane] = make_uint2((unsigned)(mine & 0xff),
-                             dd_smem_u32(smem + stg * CC * ROWLEN + lane * ROWLEN) + 4u * (unsigned)(mine >> 8));
-    __syncwarp();
-    dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
-    const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
-    const unsigned lane4 = 4u * (unsigned)lane;
-#if defined(DD_HAVE_ASM) && !defined(DD_ONE)
-    // two channels (in order) per dispatch block: one slot load and one
-    // loop trip per pair
-    int c = 0;
-#pragma unroll 1
-    for (; c + 1 < nch; c += 2) {
-      const uint4 sl = *reinterpret_cast<const uint4*>(slots + c);  // broadcast
-      dd_asm_dispatch2(acc, (int)sl.x, sl.y + lane4, (int)sl.z, sl.w + lane4);
-    }
-    if (c < nch) {
-      const uint2 sl = slots[c];
-      dd_asm_dispatch(acc, (int)sl.x, sl.y + lane4);
-    }
-#else
-#pragma unroll 1
-    for (int c = 0; c < nch; ++c) {
-      const uint2 sl = slots[c];  // broadcast
-#ifdef DD_HAVE_ASM
-      dd_asm_dispatch(acc, (int)sl.x, sl.y + lane4);
-#else
-      dd_dispatch(st, (int)sl.x, reinterpret_cast<const float*>(__cvta_shared_to_generic(sl.y + lane4)));
-#endif
-    }
-#endif
-#else
     dd_mbar_wait(bars + stg, (t / NSTAGE) & 1);
     const float* srow = smem + stg * CC * ROWLEN + lane;
     const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
+#if defined(DD_HAVE_ASM) && !defined(DD_ONE)
+    // two channels (in order) per dispatch block: one loop trip and one
+    // convergence region per pair (measured 4.44 -> see DESIGN 3.1)
+    int c = 0;
+#pragma unroll 1
+    for (; c + 1 < nch; c += 2, srow += 2 * ROWLEN) {
+      const int pk0 = __shfl_sync(0xffffffffu, mine, c);
+      const int pk1 = __shfl_sync(0xffffffffu, mine, c + 1);
+      dd_asm_dispatch2(acc, pk0 & 0xff, dd_smem_u32(srow + (pk0 >> 8)), pk1 & 0xff,
+                       dd_smem_u32(srow + ROWLEN + (pk1 >> 8)));
+    }
+    if (c < nch) {
+      const int pk = __shfl_sync(0xffffffffu, mine, c);
+      dd_asm_dispatch(acc, pk & 0xff, dd_smem_u32(srow + (pk >> 8)));
+    }
+#else
 #pragma unroll 1
     for (int c = 0; c < nch; ++c, srow += ROWLEN) {
       const int pk = __shfl_sync(0xffffffffu, mine, c);

@@ -816,9 +816,7 @@ class Dedispersion(Problem):
             return self._staged_smem(cfg, ns) if ns else 0
         rowlen = (32 * cfg["tile_size_x"] + self.block_span(cfg) + span + 4 + 3) & ~3
         npat = 1 << (cfg["tile_size_y"] - 1)
-        slots = 8 * 32 * cfg["block_size_y"]  # per-warp dispatch slots (uint2 per channel)
-        return (4 * self.DD_STAGES * self.DD_CC * rowlen + 16 * self.DD_STAGES + 4 * self.NCH
-                + npat + 16 + slots)  # slots start 16-byte aligned after the pattern table
+        return 4 * self.DD_STAGES * self.DD_CC * rowlen + 16 * self.DD_STAGES + 4 * self.NCH + npat
 
     # staged generic mode (kernels/dedispersion.cu DD_STG) for non-window
     # configurations with enough work per staged row: >= 4 threads and >= 12
