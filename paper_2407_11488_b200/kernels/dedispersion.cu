@@ -286,7 +286,9 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
     const int nch = NCH - t * CC < CC ? NCH - t * CC : CC;
 #if defined(DD_HAVE_ASM) && !defined(DD_ONE)
     // two channels (in order) per dispatch block: one loop trip and one
-    // convergence region per pair (measured 4.44 -> see DESIGN 3.1)
+    // convergence region per pair (measured: 4.44 -> 4.27 ms at (32,32,4,8,1,0),
+    // 6.05 -> 5.82 ms at (32,16,4,8,1,0); a shared-memory slot table instead
+    // of the shuffles was slower)
     int c = 0;
 #pragma unroll 1
     for (; c + 1 < nch; c += 2, srow += 2 * ROWLEN) {
