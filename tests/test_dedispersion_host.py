@@ -34,10 +34,15 @@ def test_window_eligibility_and_spans():
 def test_asm_dispatch_cases(tsx, tsy, span):
     code = dd_asm_dispatch(tsx, tsy, span)
     pats = [q for q in range(1 << (tsy - 1)) if bin(q).count("1") <= span]
-    labels = re.findall(r"L(\d+)_%=:", code)
-    assert [int(x) for x in labels] == list(range(len(pats)))
-    # adds per case = TSY x TSX/2 packed accumulators
-    assert code.count("add.rn.f32x2") == len(pats) * tsy * (tsx // 2)
+    # the single-channel block (section a) and the two-channel block
+    # (sections a, b: one dispatch per channel, in order)
+    one, two = code.split("dd_asm_dispatch2")
+    for sec, text in (("a", one), ("a", two), ("b", two)):
+        labels = re.findall(rf"L{sec}(\d+)_%=:", text)
+        assert [int(x) for x in labels] == list(range(len(pats)))
+    # adds per case = TSY x TSX/2 packed accumulators, per channel
+    assert one.count("add.rn.f32x2") == len(pats) * tsy * (tsx // 2)
+    assert two.count("add.rn.f32x2") == 2 * len(pats) * tsy * (tsx // 2)
 
 
 def test_asm_dispatch_source_compiles_for_sm100a():
