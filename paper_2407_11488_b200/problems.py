@@ -677,6 +677,8 @@ def dd_asm_dispatch(tsx: int, tsy: int, span: int) -> str:
     # two channels (in order) per asm block: the loop overhead and the
     # dispatch-slot load are paid once per pair
     two = "\\n".join(head + section("a", nacc, nacc + 1) + section("b", nacc + 2, nacc + 3) + ["}"])
+    four = "\\n".join(head + section("a", nacc, nacc + 1) + section("b", nacc + 2, nacc + 3)
+                      + section("c", nacc + 4, nacc + 5) + section("d", nacc + 6, nacc + 7) + ["}"])
     return (
         "#define DD_HAVE_ASM 1\n"
         "__device__ __forceinline__ void dd_asm_dispatch(unsigned long long (&acc)[TSY][XP], int idx, unsigned saddr) {\n"
@@ -688,6 +690,11 @@ def dd_asm_dispatch(tsx: int, tsy: int, span: int) -> str:
         "__device__ __forceinline__ void dd_asm_dispatch2(unsigned long long (&acc)[TSY][XP], int idx0, unsigned saddr0,"
         " int idx1, unsigned saddr1) {\n"
         f'  asm volatile("{two}" : {outs} : "r"(idx0), "r"(saddr0), "r"(idx1), "r"(saddr1));\n'
+        "}\n"
+        "__device__ __forceinline__ void dd_asm_dispatch4(unsigned long long (&acc)[TSY][XP], const int (&idx)[4],"
+        " const unsigned (&saddr)[4]) {\n"
+        f'  asm volatile("{four}" : {outs} : "r"(idx[0]), "r"(saddr[0]), "r"(idx[1]), "r"(saddr[1]),'
+        ' "r"(idx[2]), "r"(saddr[2]), "r"(idx[3]), "r"(saddr[3]));\n'
         "}\n")
 
 

@@ -36,13 +36,15 @@ def test_asm_dispatch_cases(tsx, tsy, span):
     pats = [q for q in range(1 << (tsy - 1)) if bin(q).count("1") <= span]
     # the single-channel block (section a) and the two-channel block
     # (sections a, b: one dispatch per channel, in order)
-    one, two = code.split("dd_asm_dispatch2")
-    for sec, text in (("a", one), ("a", two), ("b", two)):
-        labels = re.findall(rf"L{sec}(\d+)_%=:", text)
-        assert [int(x) for x in labels] == list(range(len(pats)))
-    # adds per case = TSY x TSX/2 packed accumulators, per channel
-    assert one.count("add.rn.f32x2") == len(pats) * tsy * (tsx // 2)
-    assert two.count("add.rn.f32x2") == 2 * len(pats) * tsy * (tsx // 2)
+    one, rest = code.split("dd_asm_dispatch2")
+    two, four = rest.split("dd_asm_dispatch4")
+    blocks = ((one, "a"), (two, "ab"), (four, "abcd"))  # one, two, four channels per block
+    for text, secs in blocks:
+        for sec in secs:
+            labels = re.findall(rf"L{sec}(\d+)_%=:", text)
+            assert [int(x) for x in labels] == list(range(len(pats)))
+        # adds per case = TSY x TSX/2 packed accumulators, per channel
+        assert text.count("add.rn.f32x2") == len(secs) * len(pats) * tsy * (tsx // 2)
 
 
 def test_asm_dispatch_source_compiles_for_sm100a():
