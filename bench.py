@@ -84,7 +84,7 @@ KNOWN_OPTIMUM = {"hotspot": (32, 1, 4, 1, 7, 7, 1)}
 KERNEL_SAMPLES = {
     "convolution": ([(256, 2, 4, 4, 1, 0, 0)], "tile_size_y", 11),
     "dedispersion": ([(32, 32, 4, 8, 1, 0)], "block_size_x", 7),
-    "gemm": ([(128, 64, 16, 16, 8, 16, 8, 4, 4, 1, 1, 1, 1)], "VWM", 9),
+    "gemm": ([(128, 64, 16, 8, 8, 16, 16, 4, 4, 1, 1, 1, 1)], "VWM", 9),  # whole-space optimum
     "gemm_tc": ([(256, 6, 2), (256, 4, 1)], None, 6),
 }
 
