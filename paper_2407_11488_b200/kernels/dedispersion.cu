@@ -290,20 +290,6 @@ dedispersion_kernel(float* __restrict__ out, const float* __restrict__ in, float
     // 6.05 -> 5.82 ms at (32,16,4,8,1,0); a shared-memory slot table instead
     // of the shuffles was slower)
     int c = 0;
-#ifdef DD_QUAD
-#pragma unroll 1
-    for (; c + 3 < nch; c += 4, srow += 4 * ROWLEN) {
-      int ix[4];
-      unsigned ad[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int pk = __shfl_sync(0xffffffffu, mine, c + u);
-        ix[u] = pk & 0xff;
-        ad[u] = dd_smem_u32(srow + u * ROWLEN + (pk >> 8));
-      }
-      dd_asm_dispatch4(acc, ix, ad);
-    }
-#endif
 #pragma unroll 1
     for (; c + 1 < nch; c += 2, srow += 2 * ROWLEN) {
       const int pk0 = __shfl_sync(0xffffffffu, mine, c);

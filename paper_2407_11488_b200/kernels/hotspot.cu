@@ -464,20 +464,6 @@ __device__ __forceinline__ void hs_stream_iter(const HsStream& S, float2 (&R)[TT
     const int sC = ((2 * PH - k) % 4 + 4) % 4;      // row a
     const int s0 = ((2 * PH - k + 1) % 4 + 4) % 4;  // row a+1 (fresh f0)
     const int s1 = ((2 * PH - k + 2) % 4 + 4) % 4;  // row a+2 (fresh f1)
-#ifdef HS_SKIP
-    // pipeline prologue: rows a, a+1 of level k lie below its valid band
-    // (y0 - (NS - k)) during the first iterations -- skip the arithmetic,
-    // keep the ring rotation (level k+1 is then in its garbage band too:
-    // the condition is monotone in k, so pprev is never stale when used)
-    if (i < S.y0 - NS + 2 * k - 1) {
-#pragma unroll
-      for (int q = 0; q < NP2; ++q) {
-        R[k - 1][s0][q] = f0[q];
-        R[k - 1][s1][q] = f1[q];
-      }
-      continue;
-    }
-#endif
     // E/W of the fresh centre row a+1 (row b's centre)
     float wlb = __shfl_up_sync(0xffffffffu, COL(f0, TSX - 1), 1);
     float erb = __shfl_down_sync(0xffffffffu, f0[0].x, 1);

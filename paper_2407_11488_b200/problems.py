@@ -674,11 +674,9 @@ def dd_asm_dispatch(tsx: int, tsy: int, span: int) -> str:
     head = ["{", ".reg .f32 lo, hi;"] + [f".reg .b64 w{q}_{k};" for q in range(xp) for k in range(span + 1)]
     outs = ", ".join(f'"+l"(acc[{j}][{q}])' for j in range(tsy) for q in range(xp))
     one = "\\n".join(head + section("a", nacc, nacc + 1) + ["}"])  # C string escapes: one PTX statement per line
-    # two channels (in order) per asm block: the loop overhead and the
-    # dispatch-slot load are paid once per pair
+    # two channels (in order) per asm block: the loop trip and the
+    # convergence region are paid once per pair (four per block: slower)
     two = "\\n".join(head + section("a", nacc, nacc + 1) + section("b", nacc + 2, nacc + 3) + ["}"])
-    four = "\\n".join(head + section("a", nacc, nacc + 1) + section("b", nacc + 2, nacc + 3)
-                      + section("c", nacc + 4, nacc + 5) + section("d", nacc + 6, nacc + 7) + ["}"])
     return (
         "#define DD_HAVE_ASM 1\n"
         "__device__ __forceinline__ void dd_asm_dispatch(unsigned long long (&acc)[TSY][XP], int idx, unsigned saddr) {\n"
@@ -690,11 +688,6 @@ def dd_asm_dispatch(tsx: int, tsy: int, span: int) -> str:
         "__device__ __forceinline__ void dd_asm_dispatch2(unsigned long long (&acc)[TSY][XP], int idx0, unsigned saddr0,"
         " int idx1, unsigned saddr1) {\n"
         f'  asm volatile("{two}" : {outs} : "r"(idx0), "r"(saddr0), "r"(idx1), "r"(saddr1));\n'
-        "}\n"
-        "__device__ __forceinline__ void dd_asm_dispatch4(unsigned long long (&acc)[TSY][XP], const int (&idx)[4],"
-        " const unsigned (&saddr)[4]) {\n"
-        f'  asm volatile("{four}" : {outs} : "r"(idx[0]), "r"(saddr[0]), "r"(idx[1]), "r"(saddr[1]),'
-        ' "r"(idx[2]), "r"(saddr[2]), "r"(idx[3]), "r"(saddr[3]));\n'
         "}\n")
 
 

@@ -36,9 +36,8 @@ def test_asm_dispatch_cases(tsx, tsy, span):
     pats = [q for q in range(1 << (tsy - 1)) if bin(q).count("1") <= span]
     # the single-channel block (section a) and the two-channel block
     # (sections a, b: one dispatch per channel, in order)
-    one, rest = code.split("dd_asm_dispatch2")
-    two, four = rest.split("dd_asm_dispatch4")
-    blocks = ((one, "a"), (two, "ab"), (four, "abcd"))  # one, two, four channels per block
+    one, two = code.split("dd_asm_dispatch2")
+    blocks = ((one, "a"), (two, "ab"))  # one and two channels per block
     for text, secs in blocks:
         for sec in secs:
             labels = re.findall(rf"L{sec}(\d+)_%=:", text)
