@@ -637,6 +637,22 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
+#ifdef HS_P4
+  // experiment: four iterations per loop trip (two ring periods) for the
+  // interior tiles -- more room for ptxas to coalesce the loop-carried rings
+  if (E == 0) {
+    for (int i = S.ia; i <= S.ib; i += 8) {
+      hs_stream_iter<0, E, NS>(S, R, i, kk, k2);
+      if (i + 2 > S.ib) break;
+      hs_stream_iter<1, E, NS>(S, R, i + 2, kk, k2);
+      if (i + 4 > S.ib) break;
+      hs_stream_iter<0, E, NS>(S, R, i + 4, kk, k2);
+      if (i + 6 > S.ib) break;
+      hs_stream_iter<1, E, NS>(S, R, i + 6, kk, k2);
+    }
+    return;
+  }
+#endif
   for (int i = S.ia; i <= S.ib; i += 4) {
     hs_stream_iter<0, E, NS>(S, R, i, kk, k2);
     if (i + 2 > S.ib) break;
