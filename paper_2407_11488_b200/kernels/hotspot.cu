@@ -627,6 +627,9 @@ __device__ __forceinline__ void hs_stream_run1(const HsStream& S, const HsCoef& 
 }
 
 // ---- two rows per iteration (loop_unroll_factor_t > 1) -----------------------
+#ifndef HS_P4
+#define HS_P4 ((TT) <= 7)
+#endif
 template <int E, int NS>
 __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& kk) {
   const HsK2 k2 = hs_pairs(kk);
@@ -637,9 +640,12 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
     for (int b = 0; b < 4; ++b)
 #pragma unroll
       for (int q = 0; q < NP2; ++q) R[a][b][q] = make_float2(0.f, 0.f);
-#ifdef HS_P4
-  // experiment: four iterations per loop trip (two ring periods) for the
-  // interior tiles -- more room for ptxas to coalesce the loop-carried rings
+#if HS_P4
+  // four iterations per loop trip (two ring periods) for the interior
+  // tiles: ptxas coalesces the loop-carried rings instead of emitting ~45
+  // register moves at every back edge (interior loop 626 -> 577 SASS per 4
+  // rows at T=7; measured T=7 0.1474 -> 0.1420 ms).  Only for TT <= 7: at
+  // TT = 10 the longer body spills (0.150 -> 0.199 ms), at TT = 8 it is even
   if (E == 0) {
     for (int i = S.ia; i <= S.ib; i += 8) {
       hs_stream_iter<0, E, NS>(S, R, i, kk, k2);
