@@ -67,8 +67,22 @@ def _cuda(arg, job):
     if problem.space.fingerprint() != job.space.fingerprint():
         raise ProtocolError(f"--space does not match the {arg} kernel's space "
                             f"({job.space.kernel_name} vs {problem.space.kernel_name})")
-    device = rt.Device(int(os.environ.get("LOCAL_RANK", "0")))
+    device = rt.Device(_local_device())
     return cuda_backend(CudaTarget(problem, device=device, verify=job.verify))
+
+
+def _local_device() -> int:
+    """This rank's GPU: LOCAL_RANK, wrapped over the visible GPUs (more ranks
+    than GPUs share them -- a functional test of the sharded path on a
+    one-GPU host; one rank per GPU is the measuring setup)."""
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    try:
+        import torch
+
+        n = torch.cuda.device_count()
+    except Exception:  # noqa: BLE001 -- no torch: one device per rank
+        n = 0
+    return local % n if n else local
 
 
 _BACKEND_KINDS = {"sim": _sim, "cmd": _cmd, "cuda": _cuda}
@@ -151,13 +165,9 @@ def _join_ranks(world: int, backend_spec: str):
 
     if world == 1 or dist.is_initialized():
         return
-    if backend_spec.startswith("cuda:"):
-        import torch
-
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
-        dist.init_process_group("nccl")
-    else:
-        dist.init_process_group("gloo")
+    # the sharded sweep's only inter-rank traffic is host-side (a TCPStore
+    # counter and one gather of the results): gloo, for every backend
+    dist.init_process_group("gloo")
 
 
 # ---------------------------------------------------------------------------

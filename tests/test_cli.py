@@ -165,3 +165,25 @@ def test_resume_counts_every_rank_log(golden, tmp_path):
                              resume_from=[str(base), f"{base}.rank0", f"{base}.rank1"])
     assert [c for c, _ in trace] == configs
     assert calls == []  # everything came from the logs
+
+
+@pytest.mark.gpu
+def test_tune_sharded_over_ranks_on_the_gpu(tmp_path):
+    """``--devices 2``: the command re-launches itself as two torchrun ranks
+    (on a one-GPU host both share it -- the functional path of the sharded
+    sweep: TCPStore chunk queue, gloo gather, merge by draw order); the
+    random search's pre-drawn sequence gives exactly the single-process
+    run's configurations, every one measured and verified on the device."""
+    args = ["--space", "convolution", "--backend", "cuda:convolution", "--strategy", "random",
+            "--budget", "8", "--seed", "3"]
+    one, two = tmp_path / "one.json", tmp_path / "two.json"
+    base = [sys.executable, "-m", "paper_2407_11488_b200", "tune"]
+    r1 = subprocess.run(base + args + ["--out", str(one)], capture_output=True, text=True, timeout=900)
+    assert r1.returncode == 0, r1.stderr[-2000:]
+    r2 = subprocess.run(base + args + ["--devices", "2", "--out", str(two)], capture_output=True, text=True,
+                        timeout=900)
+    assert r2.returncode == 0, r2.stderr[-2000:]
+    c1, c2 = read_cache(one), read_cache(two)
+    assert list(c1.records) == list(c2.records) and len(c2.records) == 8
+    assert all(o.ok for o in c2.records.values())
+    assert [o.status for o in c1.records.values()] == [o.status for o in c2.records.values()]
