@@ -78,7 +78,7 @@ WORKLOADS = {
 
 # headline workloads: the full-space optimum measured on a B200 (whole-space
 # sweep through the tune command line, profiles/round2/caches/*.summary.json)
-KNOWN_OPTIMUM = {"hotspot": (32, 1, 4, 1, 7, 7, 1)}
+KNOWN_OPTIMUM = {"hotspot": (8, 8, 4, 1, 7, 7, 1)}
 
 # kernels block: (known full-space optimum or best round-1 configuration, stratify-by, sample size)
 KERNEL_SAMPLES = {
