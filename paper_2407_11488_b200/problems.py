@@ -425,7 +425,7 @@ class Hotspot(Problem):
         nxe, nxi = xl + nstrips - xr, xr - xl
         warps = tsy * blocks_per_sm * wpb * n_sm  # TSY whole waves of warp tiles
         cap = self.H // max(8, 2 * t)
-        f = self.STREAM_XEDGE_F
+        f = self.STREAM_XEDGE_F or (1.5 if t <= 8 else 1.3)
         if nxi:
             ni = max(1, min(int(warps // (nxi + nxe * f)), cap))
             ne = max(1, min(math.ceil(ni * f), cap))
@@ -448,8 +448,10 @@ class Hotspot(Problem):
     STREAM_EDGE_SEG = float(os.environ.get("TSG_HS_EDGE_SEG", "0.25"))
     # border strips run the all-selects code (~1.6x the interior's
     # instructions per row, SASS loop bodies): they get this many times the
-    # interior strips' segment count (TSG_HS_XEDGE_F for experiments)
-    STREAM_XEDGE_F = float(os.environ.get("TSG_HS_XEDGE_F", "1.3"))
+    # interior strips' segment count -- 1.5 for T <= 8 (the faster
+    # four-iteration interior loop), 1.3 above (measured,
+    # profiles/round2/hs_ring/hs_exp_xe2.jsonl); TSG_HS_XEDGE_F overrides
+    STREAM_XEDGE_F = float(os.environ.get("TSG_HS_XEDGE_F", "0"))
     # programmatic dependent launch between the launches of one run
     # (TSG_HS_PDL=0 disables it for experiments)
     STREAM_PDL = os.environ.get("TSG_HS_PDL", "1") != "0"
