@@ -290,29 +290,13 @@ __device__ __forceinline__ void hs_stage_p(const HsStream& S, int row) {
 //   one row per iteration: input row i+NR-1, power row i+PD-1; iteration i
 //   first reads power row i-1 (PD groups earlier) and input row i.
 __device__ __forceinline__ void hs_stage_iter2(const HsStream& S, int i) {
-  // both rows of a pair sit in adjacent slots (even slot first: i - ia is
-  // even, so neither ring wraps inside a pair) -- one slot computation and
-  // one global row address per ring, the second row at a fixed offset
-  const int r0 = i + NR - 2;
-  const size_t rb = (size_t)r0 * GW;
-  float* tr = S.tring + ((r0 - S.ia) & (NR - 1)) * SW;
-#pragma unroll
-  for (int u = 0; u < 2; ++u)
-    if ((unsigned)(r0 + u - S.ia) <= S.nst)
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        cp_chunk(chunk_ptr(tr + u * SW, c, S.lane), S.tin + rb + u * GW + S.csrc[c], S.cbytes[c]);
-#if SH_POWER
-  const int p0 = i + PD - 1;
-  const size_t pb = (size_t)p0 * GW;
-  float* pr = S.pring + ((p0 - S.ia + 1) & (PR - 1)) * SW;
-#pragma unroll
-  for (int u = 0; u < 2; ++u)
-    if ((unsigned)(p0 + u - S.ia) <= S.nst)
-#pragma unroll
-      for (int c = 0; c < NCH; ++c)
-        cp_chunk(chunk_ptr(pr + u * SW, c, S.lane), S.power + pb + u * GW + S.csrc[c], S.cbytes[c]);
-#endif
+  // (one slot computation and row address per ring and pair instead of per
+  // row saved 3% of the T=7 loop's instructions but measured 15% slower at
+  // T=5 -- profiles/round2/hs_ring/hs_exp_t5.jsonl; kept per row)
+  hs_stage_t(S, i + NR - 2);
+  hs_stage_t(S, i + NR - 1);
+  hs_stage_p(S, i + PD - 1);
+  hs_stage_p(S, i + PD);
   cp_commit();
 }
 __device__ __forceinline__ void hs_stage_iter1(const HsStream& S, int i) {
