@@ -78,9 +78,9 @@ def test_gpu_dedispersion_cache_imports_into_reference(tmp_path, reference_pkg):
     assert build_ffg(ref, rs) is not None  # complete landscape
 
 
-# ---- round 2: the hotspot (and, once swept, GEMM) spaces -------------------
+# ---- round 2: all four spaces swept with the final kernels -----------------
 CACHES2 = Path(__file__).resolve().parents[1] / "profiles" / "round2" / "caches"
-FULL2 = {"hotspot": 105412, "gemm": 116928}
+FULL2 = {"hotspot": 105412, "gemm": 116928, "convolution": 4362, "dedispersion": 11130}
 
 
 def _unzip2(name: str, tmp_path: Path) -> Path:
