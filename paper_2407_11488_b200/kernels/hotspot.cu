@@ -648,8 +648,10 @@ __device__ __forceinline__ void hs_stream_run(const HsStream& S, const HsCoef& k
   // tiles: ptxas coalesces the loop-carried rings instead of emitting ~45
   // register moves at every back edge (interior loop 626 -> 577 SASS per 4
   // rows at T=7; measured T=7 0.1474 -> 0.1420 ms).  Only for TT <= 7: at
-  // TT = 10 the longer body spills (0.150 -> 0.199 ms), at TT = 8 it is even
-  if (E == 0) {
+  // TT = 10 the longer body spills (0.150 -> 0.199 ms), at TT = 8 it is even.
+  // Full-depth launches only (NS == TT): the single remainder launch keeps
+  // the shorter loop -- one stream-loop copy less for NVRTC per configuration
+  if (E == 0 && NS == TT) {
     for (int i = S.ia; i <= S.ib; i += 8) {
       hs_stream_iter<0, E, NS>(S, R, i, kk, k2);
       if (i + 2 > S.ib) break;
