@@ -215,7 +215,7 @@ def test_gemm_tc_tf32_within_k_scaled_tolerance(device):
     big = GemmTC()
     tgt = CudaTarget(big, device=device)
     try:
-        for c in [(256, 4, 1), (256, 2, 2)]:  # single CTA; 2-CTA cluster with multicast B
+        for c in [(256, 4, 1), (256, 6, 2)]:  # single CTA; 2-SM UMMA pair (cta_group::2)
             obs = tgt.execute(c, PROTO)
             assert obs.ok, (c, obs)
             assert tgt.extras[",".join(map(str, c))]["verify"]["max_abs_err"] <= big.abs_tol
